@@ -1,0 +1,92 @@
+// Kernel launch interfaces shared by the host-side runtime (world/protocol/capi).
+#pragma once
+#include "common.cuh"
+
+namespace chroma {
+
+void count_launch(int k = 1);
+i64 launch_count();
+
+// ---------------------------------------------------------------- colouring
+struct GsLaunch {
+  const i64* rowptr = nullptr;
+  const i32* col = nullptr;
+  i32* val = nullptr;          // colours, worklist entries preset to PENDING
+  const i32* old = nullptr;    // optional pre-call colours of worklist vertices
+  const i32* wl = nullptr;     // optional sorted unique worklist
+  i64 wl_base = 0;             // identity worklist base when wl == nullptr
+  const i64* nwl_dev = nullptr;
+  i64 nwl_max = 0;             // upper bound used to size the grid
+  const i32* prio = nullptr;   // optional ordering key
+  unsigned long long* ticket = nullptr;
+  int dist = 1;
+  bool partial = false;
+};
+void launch_gs(const GsLaunch& L, cudaStream_t s);
+
+// Jacobi sweep pieces (chroma/localcolor.py:214-227, 292-303)
+void launch_jacobi_propose(const i64* rowptr, const i32* col, const i32* colors, const i32* pending,
+                           const i64* np_dev, i64 np_max, i32* prop, int dist, bool partial,
+                           cudaStream_t s);
+void launch_jacobi_losers(const i64* rowptr, const i32* col, i32* colors, const i32* pending,
+                          const i64* np_dev, i64 np_max, const i32* prop, const uint8_t* in_round,
+                          uint8_t* lose, int dist, bool partial, cudaStream_t s);
+
+// ---------------------------------------------------------------- utilities
+void launch_fill_i32(i32* p, i64 n, i32 v, cudaStream_t s);
+void launch_iota_i32(i32* p, i64 n, i32 base, cudaStream_t s);
+void launch_scatter_const(i32* val, const i32* idx, const i64* n_dev, i64 n_max, i32 v, cudaStream_t s);
+void launch_scatter_from(i32* dst, const i32* src, const i32* idx, const i64* n_dev, i64 n_max,
+                         cudaStream_t s);
+void launch_scatter_idx_values(i32* dst, const i32* idx, const i32* values, const i64* n_dev,
+                               i64 n_max, cudaStream_t s);
+void launch_clamp_nonneg(i32* dst, const i32* src, i64 n, cudaStream_t s);
+// ordered compaction of indices i in [0,n) with flag[i] != 0; count -> *n_out (device)
+void select_flagged(const uint8_t* flags, i64 n, i32* out, i64* n_out, cudaStream_t s);
+void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* out, i64* n_out,
+                           cudaStream_t s);
+void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s);
+
+// ---------------------------------------------------------------- detection
+struct DetectArgs {
+  const i64* rowptr;
+  const i32* col;
+  i32* colors;
+  const i64* gids;
+  const i32* deg;
+  const i32* rows;    // detection rows: ghost lids (D1) / boundary_d2 lids (D2)
+  i64 nrows;
+  int dist;
+  bool partial;
+  bool recolor_degrees;
+  bool sequential;    // exact replay of the reference's in-place scan (F5)
+};
+struct DetectScratch {
+  DBuf<i64> cnt, off;
+  DBuf<int2> ev;
+  DBuf<uint8_t> fired;
+  DBuf<i32> kill;
+  DBuf<unsigned long long> result;  // [0] conflicts
+  DBuf<i64> total;
+};
+// Adds the number of conflicts to *conflicts_dev (device, unsigned long long).
+void run_detect(const DetectArgs& a, i64 num_vertices, DetectScratch& S,
+                unsigned long long* conflicts_dev, cudaStream_t s);
+
+// ---------------------------------------------------------------- exchange (device copy)
+void launch_exchange_local(const i32* routed, i64 nrouted, const i64* st_off, const i32* st_dst,
+                           const i32* st_pair, i32* colors, i32* last_sent, bool changed_only,
+                           bool write_all, unsigned long long* pair_cnt, cudaStream_t s);
+void launch_pair_stats(unsigned long long* pair_cnt, i64 npairs, unsigned long long* stats2,
+                       cudaStream_t s);
+
+// ---------------------------------------------------------------- verification
+struct VerifyResult {
+  i64 total;
+};
+i64 run_verify(const i64* rowptr, const i32* col, i64 n, const i32* colors, const uint8_t* mask,
+               int mode, i64* rows_host, i64 cap, cudaStream_t s);
+void run_color_stats(const i32* colors, i64 n, i64* num_colors, i64* max_color, i64* hist_host,
+                     i64 hist_cap, cudaStream_t s);
+
+}  // namespace chroma

@@ -1,0 +1,397 @@
+// The speculate-and-iterate round loop (chroma/protocol.py:263-334) and the local
+// colouring driver (chroma/localcolor.py:198-303), entirely device-side except for
+// one small D2H of the round's counters (and of the conflict-event count).
+//
+// Per round, per the reference:
+//   colour the worklist (round 0: every owned vertex; later: every uncoloured local
+//   vertex, F7) -> restore ghosts -> exchange (changed-only accounting, F11) ->
+//   snapshot ghosts -> detect -> allreduce -> stop on zero (F12: max_rounds+1 rounds).
+// Device formulation: the exchange rewrites every routed ghost from its owner each
+// round, which leaves every ghost equal to the owner's colour -- exactly the state
+// restore + changed-only exchange produces -- so no snapshot buffer is needed.  In
+// Gauss-Seidel mode ghost worklist entries are skipped: ghosts have larger local ids
+// than every owned vertex, so their sequential recolouring can only affect other
+// ghosts, which the restore/exchange overwrites.
+#include <chrono>
+#include <cub/cub.cuh>
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sort.h>
+#include <thrust/unique.h>
+
+#include "world.cuh"
+
+namespace chroma {
+namespace {
+
+__global__ void k_flag_worklist(const i32* colors, const uint8_t* owned_flag, i64 n, bool owned_only,
+                                uint8_t* flag) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    flag[i] = (colors[i] == 0 && (!owned_only || owned_flag[i])) ? 1 : 0;
+}
+
+// recolored_per_rank: owned entries of the worklist per local rank
+__global__ void k_count_recolored(const i32* wl, const i64* nwl, const uint8_t* owned_flag,
+                                  const i32* rank_of, i32 rank_lo, unsigned long long* stats) {
+  const i64 n = *nwl;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = wl[i];
+    if (owned_flag[v]) atomicAdd(&stats[3 + rank_lo + rank_of[v]], 1ull);
+  }
+}
+
+__global__ void k_set_u8_idx(uint8_t* flags, const i32* idx, const i64* n_dev, uint8_t v) {
+  const i64 n = *n_dev;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    flags[idx[i]] = v;
+}
+
+__global__ void k_gather_owned(const i64* gids, const i32* colors, i64 lo, i64 n, i32* out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[gids[lo + i]] = colors[lo + i];
+}
+
+int G(i64 n) { return grid_for(std::max<i64>(n, 1), 256, num_sms() * 16); }
+
+i64 read_i64(const i64* d, cudaStream_t s) {
+  i64 h = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  return h;
+}
+
+constexpr int MAX_SWEEPS = 10000;  // chroma/localcolor.py:34
+
+}  // namespace
+
+// ------------------------------------------------------------------ colouring driver
+void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32* wl_in,
+               const i64* nwl_dev, i64 nwl_max, bool wl_sorted_unique, int dist, bool partial,
+               int algo, bool colors_nonneg, ColorScratch& S, cudaStream_t s) {
+  if (nwl_max <= 0) return;
+  S.nwl.reserve(1, s);
+  S.ticket.reserve(1, s);
+  const i32* wl = wl_in;
+  const i64* nwl = nwl_dev;
+  if (!wl_sorted_unique) {
+    // the reference sorts the worklist (np.sort); duplicates are idempotent
+    S.wl.reserve(nwl_max, s);
+    CUDA_CHECK(cudaMemcpyAsync(S.wl.p, wl_in, sizeof(i32) * nwl_max, cudaMemcpyDeviceToDevice, s));
+    auto b = thrust::device_pointer_cast(S.wl.p);
+    thrust::sort(thrust::cuda::par.on(s), b, b + nwl_max);
+    const i64 k = thrust::unique(thrust::cuda::par.on(s), b, b + nwl_max) - b;
+    count_launch(2);
+    CUDA_CHECK(cudaMemcpyAsync(S.nwl.p, &k, sizeof(i64), cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    wl = S.wl.p;
+    nwl = S.nwl.p;
+    nwl_max = k;
+  }
+  if (algo == CHROMA_ALGO_GAUSS_SEIDEL || algo == CHROMA_ALGO_FREE) {
+    GsLaunch L;
+    L.rowptr = rowptr;
+    L.col = col;
+    if (colors_nonneg) {
+      // protocol path: worklist colours are 0 and no colour is negative
+      L.val = colors;
+      L.old = nullptr;
+      launch_scatter_const(colors, wl, nwl, nwl_max, PENDING, s);
+    } else {
+      S.val.reserve(nv, s);
+      S.old.reserve(nv, s);
+      CUDA_CHECK(cudaMemcpyAsync(S.old.p, colors, sizeof(i32) * nv, cudaMemcpyDeviceToDevice, s));
+      launch_clamp_nonneg(S.val.p, colors, nv, s);
+      launch_scatter_const(S.val.p, wl, nwl, nwl_max, PENDING, s);
+      L.val = S.val.p;
+      L.old = S.old.p;
+    }
+    L.wl = wl;
+    L.nwl_dev = nwl;
+    L.nwl_max = nwl_max;
+    L.ticket = S.ticket.p;
+    L.dist = dist;
+    L.partial = partial;
+    launch_gs(L, s);
+    if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
+    return;
+  }
+  // Jacobi sweeps (chroma/localcolor.py:214-227, 292-303)
+  S.in_round.reserve(nv, s);
+  CUDA_CHECK(cudaMemsetAsync(S.in_round.p, 0, nv, s));
+  k_set_u8_idx<<<G(nwl_max), 256, 0, s>>>(S.in_round.p, wl, nwl, 1);
+  count_launch();
+  S.prop.reserve(nwl_max, s);
+  S.flags.reserve(nwl_max, s);
+  S.pend2.reserve(nwl_max, s);
+  S.np2.reserve(1, s);
+  S.val.reserve(nwl_max, s);
+  CUDA_CHECK(cudaMemcpyAsync(S.val.p, wl, sizeof(i32) * nwl_max, cudaMemcpyDeviceToDevice, s));
+  CUDA_CHECK(cudaMemcpyAsync(S.np2.p, nwl, sizeof(i64), cudaMemcpyDeviceToDevice, s));
+  i32* pend = S.val.p;
+  i64 np = read_i64(nwl, s);  // exact count: the compaction below takes a host length
+  for (int sweep = 0; sweep < MAX_SWEEPS; sweep++) {
+    if (np == 0) return;
+    launch_jacobi_propose(rowptr, col, colors, pend, S.np2.p, np, S.prop.p, dist, partial, s);
+    launch_jacobi_losers(rowptr, col, colors, pend, S.np2.p, np, S.prop.p, S.in_round.p, S.flags.p,
+                         dist, partial, s);
+    select_flagged_values(pend, S.flags.p, np, S.pend2.p, S.np2.p, s);
+    np = read_i64(S.np2.p, s);
+    launch_scatter_const(colors, S.pend2.p, S.np2.p, np, 0, s);
+    std::swap(S.pend2, S.val);
+    pend = S.val.p;
+  }
+  // the reference raises after the last sweep even if it settled (chroma/localcolor.py:218-227)
+  throw Error(CHROMA_ERUNTIME, "speculative loop failed to settle");
+}
+
+// ------------------------------------------------------------------ remote exchange
+namespace {
+__global__ void k_changed(const i32* routed, i64 n, const i32* colors, i32* last_sent, bool changed_only,
+                          uint8_t* changed) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = routed[i];
+    const i32 c = colors[v];
+    const bool send = !changed_only || last_sent[i] != c;
+    if (send) last_sent[i] = c;
+    changed[v] = send ? 1 : 0;
+  }
+}
+__global__ void k_pack(const i32* send_lids, const i32* send_peer, i64 n, const i32* colors,
+                       const uint8_t* changed, i32* buf, unsigned long long* peer_cnt) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = send_lids[i];
+    buf[i] = colors[v];
+    if (changed[v]) atomicAdd(&peer_cnt[send_peer[i]], 1ull);
+  }
+}
+__global__ void k_unpack(const i32* recv_lids, i64 n, const i32* buf, i32* colors) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    colors[recv_lids[i]] = buf[i];
+}
+}  // namespace
+
+#ifdef CHROMA_WITH_NCCL
+#define NCCL_CHECK(expr)                                                                        \
+  do {                                                                                          \
+    ncclResult_t _r = (expr);                                                                   \
+    if (_r != ncclSuccess) throw Error(CHROMA_ECUDA, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+#endif
+
+// Pack -> grouped NCCL send/recv over NVLink -> unpack, with the reference's
+// changed-only accounting of this rank's sends added to stats[1..2].
+static void exchange_remote(World& w, bool changed_only) {
+#ifdef CHROMA_WITH_NCCL
+  cudaStream_t s = w.stream;
+  if (w.nrouted_remote)
+    k_changed<<<G(w.nrouted_remote), 256, 0, s>>>(w.routed_remote.p, w.nrouted_remote, w.colors.p,
+                                                   w.last_sent_remote.p, changed_only, w.changed.p);
+  if (w.nsend)
+    k_pack<<<G(w.nsend), 256, 0, s>>>(w.send_lids.p, w.send_peer.p, w.nsend, w.colors.p, w.changed.p,
+                                       w.sendbuf.p, w.pair_cnt.p);
+  count_launch(2);
+  NCCL_CHECK(ncclGroupStart());
+  for (i32 p = 0; p < w.P; p++) {
+    if (p == w.my_rank) continue;
+    if (w.send_cnt[p]) NCCL_CHECK(ncclSend(w.sendbuf.p + w.send_off[p], w.send_cnt[p], ncclInt32, p, w.comm, s));
+    if (w.recv_cnt[p]) NCCL_CHECK(ncclRecv(w.recvbuf.p + w.recv_off[p], w.recv_cnt[p], ncclInt32, p, w.comm, s));
+  }
+  NCCL_CHECK(ncclGroupEnd());
+  if (w.nrecv) {
+    k_unpack<<<G(w.nrecv), 256, 0, s>>>(w.recv_lids.p, w.nrecv, w.recvbuf.p, w.colors.p);
+    count_launch();
+  }
+  launch_pair_stats(w.pair_cnt.p, w.P, w.stats.p + 1, s);
+  CUDA_CHECK(cudaGetLastError());
+#else
+  (void)w; (void)changed_only;
+  throw Error(CHROMA_ECUDA, "built without NCCL");
+#endif
+}
+
+// ------------------------------------------------------------------ round loop
+int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* colors_out,
+                    chroma_round_report* reports, i64* recolored, i64 cap, i64* n_reports,
+                    bool out_on_device) {
+  const int need = mode == CHROMA_MODE_D1 ? 1 : 2;
+  CHROMA_REQUIRE(w.gl >= need, CHROMA_EVALUE, "mode needs more ghost layers than the world was built with");
+  CHROMA_REQUIRE(max_rounds >= 1, CHROMA_EVALUE, "max_rounds must be >= 1");
+  CHROMA_REQUIRE(w.all_local() || w.connected || w.P == 1, CHROMA_EVALUE,
+                 "world holds a subset of ranks: call chroma_world_connect first");
+  CUDA_CHECK(cudaSetDevice(w.device));
+  cudaStream_t s = w.stream;
+  const bool d2 = mode >= CHROMA_MODE_D2;
+  const bool partial = mode == CHROMA_MODE_PD2;
+  const int dist = d2 ? 2 : 1;
+  const bool gs = algo == CHROMA_ALGO_GAUSS_SEIDEL;
+  world_reset_exchange(w);
+  w.colors.zero(s);
+  w.cs.wl.reserve(w.NL + 1, s);
+  w.cs.nwl.reserve(1, s);
+  w.cs.flags.reserve(w.NL + 1, s);
+  const i64 nstats = 3 + w.P;
+  std::vector<unsigned long long> hs((size_t)nstats);
+  cudaEvent_t ev[4];
+  for (auto& e : ev) CUDA_CHECK(cudaEventCreate(&e));
+  int status = CHROMA_OK;
+  i64 round = 0;
+  DetectArgs da;
+  da.rowptr = w.g.rowptr.p;
+  da.col = w.g.col.p;
+  da.colors = w.colors.p;
+  da.gids = w.gids.p;
+  da.deg = w.deg.p;
+  da.rows = d2 ? w.b2.p : w.ghosts.p;
+  da.nrows = d2 ? w.NB2 : w.NGHOST;
+  da.dist = dist;
+  da.partial = partial;
+  da.recolor_degrees = rd;
+  da.sequential = algo != CHROMA_ALGO_FREE;
+  const bool remote = w.connected && w.P > 1;
+  for (;;) {
+    if (round > max_rounds) {
+      status = CHROMA_ENONCONV;
+      break;
+    }
+    if (round >= cap) {
+      status = CHROMA_ERUNTIME;
+      break;
+    }
+    CUDA_CHECK(cudaMemsetAsync(w.stats.p, 0, sizeof(unsigned long long) * nstats, s));
+    CUDA_CHECK(cudaEventRecord(ev[0], s));
+    // worklist (ordered compaction: ascending local id)
+    k_flag_worklist<<<G(w.NL), 256, 0, s>>>(w.colors.p, w.owned_flag.p, w.NL, round == 0 || gs, w.cs.flags.p);
+    count_launch();
+    select_flagged(w.cs.flags.p, w.NL, w.cs.wl.p, w.cs.nwl.p, s);
+    k_count_recolored<<<G(w.NL), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
+                                              w.stats.p);
+    count_launch();
+    color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, w.NL, true, dist, partial,
+              algo, true, w.cs, s);
+    CUDA_CHECK(cudaEventRecord(ev[1], s));
+    // exchange: every ghost takes its owner's colour; accounting is changed-only
+    if (w.nrouted) {
+      world_exchange_local(w, round > 0, true);
+      launch_pair_stats(w.pair_cnt.p, (i64)w.P * w.P, w.stats.p + 1, s);
+    }
+    if (remote) exchange_remote(w, round > 0);
+    CUDA_CHECK(cudaEventRecord(ev[2], s));
+    run_detect(da, w.NL, w.det, w.stats.p, s);
+#ifdef CHROMA_WITH_NCCL
+    if (remote)
+      NCCL_CHECK(ncclAllReduce(w.stats.p, w.stats.p, nstats, ncclUint64, ncclSum, w.comm, s));
+#endif
+    CUDA_CHECK(cudaEventRecord(ev[3], s));
+    CUDA_CHECK(cudaMemcpyAsync(hs.data(), w.stats.p, sizeof(unsigned long long) * nstats,
+                               cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    float t01 = 0, t12 = 0, t23 = 0;
+    cudaEventElapsedTime(&t01, ev[0], ev[1]);
+    cudaEventElapsedTime(&t12, ev[1], ev[2]);
+    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    chroma_round_report& R = reports[round];
+    R.round_index = round;
+    R.conflicts = (int64_t)hs[0];
+    R.bytes_sent = (int64_t)hs[1];
+    R.messages_sent = (int64_t)hs[2];
+    R.time_color_s = t01 * 1e-3;
+    R.time_comm_s = t12 * 1e-3;
+    R.time_detect_s = t23 * 1e-3;
+    for (i32 r = 0; r < w.P; r++) recolored[round * w.P + r] = (i64)hs[(size_t)(3 + r)];
+    round++;
+    if (hs[0] == 0) break;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  *n_reports = round;
+  if (status == CHROMA_OK && colors_out) {
+    if (w.all_local()) {
+      DBuf<i32> out;
+      i32* dst = colors_out;
+      if (!out_on_device) {
+        out.alloc(w.n_global + 1, s);
+        dst = out.p;
+      }
+      for (auto& m : w.ranks) {
+        k_gather_owned<<<G(m.owned), 256, 0, s>>>(w.gids.p, w.colors.p, m.lid_off, m.owned, dst);
+        count_launch();
+      }
+      if (!out_on_device)
+        CUDA_CHECK(cudaMemcpyAsync(colors_out, out.p, sizeof(i32) * w.n_global, cudaMemcpyDeviceToHost, s));
+    } else {
+      const RankMeta& m = w.ranks[0];
+      CUDA_CHECK(cudaMemcpyAsync(colors_out, w.colors.p + m.lid_off, sizeof(i32) * m.owned,
+                                 out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  return status;
+}
+
+// ------------------------------------------------------------------ connect (NCCL)
+#ifdef CHROMA_WITH_NCCL
+// Install the static halo routing computed by the host (dist.build_routing: ghost
+// slots grouped by owner; owned lids each peer asked for) and create this rank's
+// NCCL communicator.  All lists are in local ids of this process's single rank.
+void world_connect(World& w, const void* id_bytes, i32 nranks, i32 rank, const i64* send_counts,
+                   const i64* send_lids, const i64* recv_counts, const i64* recv_lids) {
+  CHROMA_REQUIRE(nranks == w.P, CHROMA_EVALUE, "communicator size differs from num_ranks");
+  CHROMA_REQUIRE(w.rank_hi - w.rank_lo == 1 && w.rank_lo == rank, CHROMA_EVALUE,
+                 "connected worlds hold exactly their own rank");
+  CUDA_CHECK(cudaSetDevice(w.device));
+  cudaStream_t s = w.stream;
+  const RankMeta& m = w.ranks[0];
+  const i32 P = w.P;
+  w.send_cnt.assign(send_counts, send_counts + P);
+  w.recv_cnt.assign(recv_counts, recv_counts + P);
+  CHROMA_REQUIRE(w.send_cnt[(size_t)rank] == 0 && w.recv_cnt[(size_t)rank] == 0, CHROMA_EPROTOCOL,
+                 "a rank cannot route to itself");
+  w.send_off.assign((size_t)P + 1, 0);
+  w.recv_off.assign((size_t)P + 1, 0);
+  for (i32 p = 0; p < P; p++) {
+    w.send_off[(size_t)p + 1] = w.send_off[(size_t)p] + w.send_cnt[(size_t)p];
+    w.recv_off[(size_t)p + 1] = w.recv_off[(size_t)p] + w.recv_cnt[(size_t)p];
+  }
+  w.nsend = w.send_off[(size_t)P];
+  w.nrecv = w.recv_off[(size_t)P];
+  CHROMA_REQUIRE(w.nrecv == m.ghost, CHROMA_EPROTOCOL, "every ghost slot must be received exactly once");
+  std::vector<i32> sl((size_t)w.nsend), sp((size_t)w.nsend), rl((size_t)w.nrecv);
+  std::vector<uint8_t> routed((size_t)m.owned + 1, 0), seen((size_t)m.ghost + 1, 0);
+  for (i32 p = 0; p < P; p++)
+    for (i64 k = w.send_off[(size_t)p]; k < w.send_off[(size_t)p + 1]; k++) {
+      const i64 v = send_lids[k];
+      CHROMA_REQUIRE(v >= 0 && v < m.owned, CHROMA_EPROTOCOL, "send list names a vertex this rank does not own");
+      sl[(size_t)k] = (i32)(m.lid_off + v);
+      sp[(size_t)k] = p;
+      routed[(size_t)v] = 1;
+    }
+  for (i64 k = 0; k < w.nrecv; k++) {
+    const i64 v = recv_lids[k];
+    CHROMA_REQUIRE(v >= m.owned && v < m.owned + m.ghost && !seen[(size_t)(v - m.owned)], CHROMA_EPROTOCOL,
+                   "receive list must cover each ghost slot once");
+    seen[(size_t)(v - m.owned)] = 1;
+    rl[(size_t)k] = (i32)(m.lid_off + v);
+  }
+  std::vector<i32> rt;
+  for (i64 v = 0; v < m.owned; v++)
+    if (routed[(size_t)v]) rt.push_back((i32)(m.lid_off + v));
+  w.nrouted_remote = (i64)rt.size();
+  w.routed_remote.upload(rt.data(), std::max<i64>(w.nrouted_remote, 1), s);
+  w.last_sent_remote.alloc(std::max<i64>(w.nrouted_remote, 1), s);
+  w.send_lids.upload(sl.data(), std::max<i64>(w.nsend, 1), s);
+  w.send_peer.upload(sp.data(), std::max<i64>(w.nsend, 1), s);
+  w.recv_lids.upload(rl.data(), std::max<i64>(w.nrecv, 1), s);
+  w.sendbuf.alloc(std::max<i64>(w.nsend, 1), s);
+  w.recvbuf.alloc(std::max<i64>(w.nrecv, 1), s);
+  CUDA_CHECK(cudaMemsetAsync(w.changed.p, 0, w.NL + 1, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  ncclUniqueId id;
+  std::memcpy(&id, id_bytes, sizeof(id));
+  NCCL_CHECK(ncclCommInitRank(&w.comm, nranks, id, rank));
+  w.my_rank = rank;
+  w.connected = true;
+  world_reset_exchange(w);
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+#endif
+
+}  // namespace chroma

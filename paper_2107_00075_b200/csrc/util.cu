@@ -1,0 +1,136 @@
+// Small device utilities: fills, scatters, ordered compaction, scans.
+#include <atomic>
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "kernels.cuh"
+
+namespace chroma {
+
+static std::atomic<long long> g_launches{0};
+void count_launch(int k) { g_launches += k; }
+i64 launch_count() { return (i64)g_launches.load(); }
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+namespace {
+__global__ void k_fill(i32* p, i64 n, i32 v) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) p[i] = v;
+}
+__global__ void k_iota(i32* p, i64 n, i32 base) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    p[i] = base + (i32)i;
+}
+__global__ void k_scatter_const(i32* val, const i32* idx, const i64* n_dev, i32 v) {
+  const i64 n = *n_dev;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    val[idx[i]] = v;
+}
+__global__ void k_scatter_from(i32* dst, const i32* src, const i32* idx, const i64* n_dev) {
+  const i64 n = *n_dev;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 x = idx[i];
+    dst[x] = src[x];
+  }
+}
+__global__ void k_scatter_values(i32* dst, const i32* idx, const i32* values, const i64* n_dev) {
+  const i64 n = *n_dev;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    dst[idx[i]] = values[i];
+}
+__global__ void k_clamp(i32* dst, const i32* src, i64 n) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 c = src[i];
+    dst[i] = c < 0 ? 0 : c;
+  }
+}
+}  // namespace
+
+static int ew_grid(i64 n) { return grid_for(n, 256, num_sms() * 16); }
+
+void launch_fill_i32(i32* p, i64 n, i32 v, cudaStream_t s) {
+  if (n <= 0) return;
+  k_fill<<<ew_grid(n), 256, 0, s>>>(p, n, v);
+  count_launch();
+}
+void launch_iota_i32(i32* p, i64 n, i32 base, cudaStream_t s) {
+  if (n <= 0) return;
+  k_iota<<<ew_grid(n), 256, 0, s>>>(p, n, base);
+  count_launch();
+}
+void launch_scatter_const(i32* val, const i32* idx, const i64* n_dev, i64 n_max, i32 v, cudaStream_t s) {
+  if (n_max <= 0) return;
+  k_scatter_const<<<ew_grid(n_max), 256, 0, s>>>(val, idx, n_dev, v);
+  count_launch();
+}
+void launch_scatter_from(i32* dst, const i32* src, const i32* idx, const i64* n_dev, i64 n_max,
+                         cudaStream_t s) {
+  if (n_max <= 0) return;
+  k_scatter_from<<<ew_grid(n_max), 256, 0, s>>>(dst, src, idx, n_dev);
+  count_launch();
+}
+void launch_scatter_idx_values(i32* dst, const i32* idx, const i32* values, const i64* n_dev,
+                               i64 n_max, cudaStream_t s) {
+  if (n_max <= 0) return;
+  k_scatter_values<<<ew_grid(n_max), 256, 0, s>>>(dst, idx, values, n_dev);
+  count_launch();
+}
+void launch_clamp_nonneg(i32* dst, const i32* src, i64 n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_clamp<<<ew_grid(n), 256, 0, s>>>(dst, src, n);
+  count_launch();
+}
+
+// Scratch for cub temporaries (grow-only, per thread of control; intentionally
+// never destroyed so no free runs after the CUDA context is gone).
+static DBuf<uint8_t>& cub_tmp() {
+  static thread_local DBuf<uint8_t>* b = new DBuf<uint8_t>();
+  return *b;
+}
+#define t_cub_tmp cub_tmp()
+
+void select_flagged(const uint8_t* flags, i64 n, i32* out, i64* n_out, cudaStream_t s) {
+  if (n <= 0) {
+    CUDA_CHECK(cudaMemsetAsync(n_out, 0, sizeof(i64), s));
+    return;
+  }
+  thrust::counting_iterator<i32> it(0);
+  size_t bytes = 0;
+  CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, n_out, n, s));
+  t_cub_tmp.reserve((i64)bytes, s);
+  CUDA_CHECK(cub::DeviceSelect::Flagged(t_cub_tmp.p, bytes, it, flags, out, n_out, n, s));
+  count_launch();
+}
+
+void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* out, i64* n_out,
+                           cudaStream_t s) {
+  if (n <= 0) {
+    CUDA_CHECK(cudaMemsetAsync(n_out, 0, sizeof(i64), s));
+    return;
+  }
+  size_t bytes = 0;
+  CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, bytes, values, flags, out, n_out, n, s));
+  t_cub_tmp.reserve((i64)bytes, s);
+  CUDA_CHECK(cub::DeviceSelect::Flagged(t_cub_tmp.p, bytes, values, flags, out, n_out, n, s));
+  count_launch();
+}
+
+void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s) {
+  if (n <= 0) return;
+  size_t bytes = 0;
+  CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+  t_cub_tmp.reserve((i64)bytes, s);
+  CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t_cub_tmp.p, bytes, in, out, n, s));
+  count_launch();
+}
+
+}  // namespace chroma

@@ -1,0 +1,522 @@
+// build_local_graphs on the GPU (chroma/runtime.py:149-268).
+//
+// Exact layout (F8): local ids are [owned ascending gid | layer-1 ghosts ascending
+// gid | layer-2 ghosts ascending gid]; every row is sorted by local id.
+// Row content (F10): owned rows are complete; with one ghost layer a ghost row
+// holds only its back-edges to owned vertices; with two layers layer-1 rows are
+// complete and layer-2 rows hold only back-edges to layer 1.
+//
+// No sort is needed for the rows: the global rows are gid-sorted and the local id
+// is monotone in gid inside each of the three classes, so a stable three-way
+// partition of each row by class (owned < L1 < L2) is the lid-sorted row.  The
+// class lists themselves come out sorted from an ordered compaction over gids.
+#include <algorithm>
+#include <numeric>
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sort.h>
+#include <thrust/iterator/zip_iterator.h>
+
+#include "world.cuh"
+
+namespace chroma {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__global__ void k_i64_to_i32(const i64* in, i32* out, i64 n) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = (i32)in[i];
+}
+
+__global__ void k_flag_eq_i32(const i32* a, i64 n, i32 v, uint8_t* flag) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    flag[i] = a[i] == v ? 1 : 0;
+}
+__global__ void k_flag_eq_u8(const uint8_t* a, i64 n, uint8_t v, uint8_t* flag) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    flag[i] = a[i] == v ? 1 : 0;
+}
+
+// lid_of[list[i]] = base + i ; cls[list[i]] = c
+__global__ void k_assign(const i32* list, i64 k, i32 base, uint8_t c, i32* lid_of, uint8_t* cls) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < k; i += (i64)gridDim.x * blockDim.x) {
+    lid_of[list[i]] = base + (i32)i;
+    cls[list[i]] = c;
+  }
+}
+
+// For every row of `list`, neighbours u with cls[u] == 0 get cls[u] = to.
+__global__ void k_mark_nbrs(const i32* list, i64 k, const i64* goff, const i32* gcol, uint8_t* cls,
+                            uint8_t to) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 i = warp; i < k; i += nwarps) {
+    const i32 g = list[i];
+    for (i64 e = goff[g] + lane; e < goff[g + 1]; e += 32) {
+      const i32 u = gcol[e];
+      if (cls[u] == 0) cls[u] = to;
+    }
+  }
+}
+
+// Which neighbours a local row keeps (chroma/runtime.py:186-200).
+__device__ __forceinline__ bool keep_nbr(i64 lid, i64 oc, i64 l1, int gl, uint8_t cu) {
+  if (lid < oc) return true;
+  if (lid < oc + l1) return gl == 2 || cu == 1;
+  return cu == 2;
+}
+
+__global__ void k_rowlen(const i32* lgids, i64 nl, i64 oc, i64 l1, int gl, const i64* goff,
+                         const i32* gcol, const uint8_t* cls, i64* len) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 lid = warp; lid < nl; lid += nwarps) {
+    const i32 g = lgids[lid];
+    const i64 rs = goff[g], re = goff[g + 1];
+    i64 c = 0;
+    if (lid < oc || (lid < oc + l1 && gl == 2)) {
+      c = re - rs;
+    } else {
+      for (i64 e0 = rs; e0 < re; e0 += 32) {
+        const i64 e = e0 + lane;
+        const bool k = e < re && keep_nbr(lid, oc, l1, gl, cls[gcol[e]]);
+        c += __popc(__ballot_sync(FULL, k));
+      }
+    }
+    if (lane == 0) len[lid] = c;
+  }
+}
+
+// Stable three-way partition of each kept row by class -> lid-sorted local row.
+__global__ void k_fill(const i32* lgids, i64 nl, i64 oc, i64 l1, int gl, const i64* goff,
+                       const i32* gcol, const uint8_t* cls, const i32* lid_of, const i64* lrow,
+                       i32* lcol) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 lid = warp; lid < nl; lid += nwarps) {
+    const i32 g = lgids[lid];
+    const i64 rs = goff[g], re = goff[g + 1];
+    i64 pos = lrow[lid];
+    for (uint8_t c = 1; c <= 3; c++) {
+      for (i64 e0 = rs; e0 < re; e0 += 32) {
+        const i64 e = e0 + lane;
+        bool k = false;
+        i32 u = 0;
+        if (e < re) {
+          u = gcol[e];
+          const uint8_t cu = cls[u];
+          k = cu == c && keep_nbr(lid, oc, l1, gl, cu);
+        }
+        const unsigned b = __ballot_sync(FULL, k);
+        if (k) lcol[pos + __popc(b & lanemask_lt())] = lid_of[u];
+        pos += __popc(b);
+      }
+    }
+  }
+}
+
+// boundary_d1 / edge counts (chroma/runtime.py:204-217)
+__global__ void k_bound1(const i64* lrow, const i32* lcol, i64 nl, i64 oc, uint8_t* b1,
+                         unsigned long long* ecount) {
+  unsigned long long el = 0, eg = 0;
+  for (i64 v = blockIdx.x * (i64)blockDim.x + threadIdx.x; v < nl; v += (i64)gridDim.x * blockDim.x) {
+    const i64 rs = lrow[v], re = lrow[v + 1];
+    if (v < oc) {
+      // rows are lid-sorted: owned neighbours form a prefix
+      i64 lo = rs, hi = re;
+      while (lo < hi) {
+        const i64 mid = (lo + hi) >> 1;
+        if (lcol[mid] < oc) lo = mid + 1; else hi = mid;
+      }
+      el += (unsigned long long)(lo - rs);
+      eg += (unsigned long long)(re - lo);
+      b1[v] = (re > lo) ? 1 : 0;
+    } else {
+      eg += (unsigned long long)(re - rs);
+    }
+  }
+  atomicAdd(&ecount[0], el);
+  atomicAdd(&ecount[1], eg);
+}
+
+// boundary_d2 = boundary_d1 u owned vertices with an owned boundary_d1 neighbour
+__global__ void k_bound2(const i64* lrow, const i32* lcol, i64 oc, const uint8_t* b1, uint8_t* b2) {
+  for (i64 v = blockIdx.x * (i64)blockDim.x + threadIdx.x; v < oc; v += (i64)gridDim.x * blockDim.x) {
+    uint8_t f = b1[v];
+    for (i64 e = lrow[v]; !f && e < lrow[v + 1]; e++) {
+      const i32 u = lcol[e];
+      if (u >= oc) break;
+      f = b1[u];
+    }
+    b2[v] = f;
+  }
+}
+
+__global__ void k_local_meta(const i32* lgids, i64 nl, i64 oc, const i64* goff, const i32* owner,
+                             i64* gids_out, i32* deg_out, i32* ghost_owner_out) {
+  for (i64 lid = blockIdx.x * (i64)blockDim.x + threadIdx.x; lid < nl; lid += (i64)gridDim.x * blockDim.x) {
+    const i32 g = lgids[lid];
+    gids_out[lid] = g;
+    deg_out[lid] = (i32)(goff[g + 1] - goff[g]);
+    if (lid >= oc) ghost_owner_out[lid - oc] = owner[g];
+  }
+}
+
+__global__ void k_reset(const i32* lgids, i64 nl, i32* lid_of, uint8_t* cls) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nl; i += (i64)gridDim.x * blockDim.x) {
+    lid_of[lgids[i]] = -1;
+    cls[lgids[i]] = 0;
+  }
+}
+
+__global__ void k_shift_i64(const i64* in, i64* out, i64 n, i64 add) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = in[i] + add;
+}
+__global__ void k_shift_i32(const i32* in, i32* out, i64 n, i32 add) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = in[i] + add;
+}
+__global__ void k_ghost_lids(i32* out, i64 n, i32 first) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = first + (i32)i;
+}
+__global__ void k_set_range_u8(uint8_t* p, i64 lo, i64 hi, uint8_t v) {
+  for (i64 i = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i < hi; i += (i64)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void k_set_range_i32(i32* p, i64 lo, i64 hi, i32 v) {
+  for (i64 i = lo + blockIdx.x * (i64)blockDim.x + threadIdx.x; i < hi; i += (i64)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// One route per ghost slot of every local rank: src lid (owner side), dst lid, pair id.
+__global__ void k_routes(const i64* gids, const i32* ghost_owner, i64 first_ghost_lid, i64 nghost,
+                         const i32* owned_lid, const i64* rank_lid_off, i32 dst_rank, i32 P,
+                         i32* src, i32* dst, i32* pair) {
+  for (i64 s = blockIdx.x * (i64)blockDim.x + threadIdx.x; s < nghost; s += (i64)gridDim.x * blockDim.x) {
+    const i64 lid = first_ghost_lid + s;
+    const i32 o = ghost_owner[s];
+    src[s] = (i32)(rank_lid_off[o] + owned_lid[gids[lid]]);
+    dst[s] = (i32)lid;
+    pair[s] = o * P + dst_rank;
+  }
+}
+
+__global__ void k_route_heads(const i32* src, i64 n, uint8_t* head) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || src[i] != src[i - 1]) ? 1 : 0;
+}
+__global__ void k_route_off(const i32* head_pos, const i64* nheads, i64 n, i64* off) {
+  const i64 k = *nheads;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i <= k; i += (i64)gridDim.x * blockDim.x)
+    off[i] = i < k ? head_pos[i] : n;
+}
+__global__ void k_gather_i32(const i32* src, const i32* idx, const i64* n_dev, i32* out) {
+  const i64 n = *n_dev;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = src[idx[i]];
+}
+
+int G(i64 n) { return grid_for(std::max<i64>(n, 1), 256, num_sms() * 16); }
+int GW(i64 n) { return grid_for(std::max<i64>(n, 1) * 32, 256, num_sms() * 16); }
+
+struct RankTmp {
+  RankMeta m;
+  DBuf<i32> lgids;
+  DBuf<i64> lrow;
+  DBuf<i32> lcol;
+  DBuf<i64> gids;
+  DBuf<i32> deg, ghost_owner, b1, b2;
+};
+
+}  // namespace
+
+World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32* h_owner, i32 gl,
+                    i32 lo, i32 hi, int device) {
+  CHROMA_REQUIRE(gl == 1 || gl == 2, CHROMA_EVALUE, "ghost_layers must be 1 or 2");
+  CHROMA_REQUIRE(P >= 1, CHROMA_EVALUE, "num_ranks must be >= 1");
+  CHROMA_REQUIRE(n >= 0 && n < ((i64)1 << 31) - 1, CHROMA_EVALUE, "graph too large for int32 local ids");
+  CHROMA_REQUIRE(0 <= lo && lo < hi && hi <= P, CHROMA_EVALUE, "bad local rank range");
+  const i64 nnz = h_off[n];
+  // partition validation (chroma/partition.py:36-43, chroma/runtime.py:159-161)
+  std::vector<i32> owner_v((size_t)n);
+  std::vector<i64> counts((size_t)P, 0);
+  for (i64 v = 0; v < n; v++) {
+    const i32 o = h_owner ? h_owner[v] : (i32)0;
+    CHROMA_REQUIRE(o >= 0 && o < P, CHROMA_EVALUE, "owner out of range");
+    owner_v[(size_t)v] = o;
+    counts[(size_t)o]++;
+  }
+  if (P <= n)
+    for (i32 r = 0; r < P; r++)
+      CHROMA_REQUIRE(counts[(size_t)r] > 0, CHROMA_EVALUE, "empty rank with num_ranks <= num_vertices");
+  std::vector<i32> owned_lid_h((size_t)n);
+  {
+    std::vector<i64> c((size_t)P, 0);
+    for (i64 v = 0; v < n; v++) owned_lid_h[(size_t)v] = (i32)c[(size_t)owner_v[(size_t)v]]++;
+  }
+  i64 dmax = 0;
+  for (i64 v = 0; v < n; v++) dmax = std::max(dmax, h_off[v + 1] - h_off[v]);
+
+  CUDA_CHECK(cudaSetDevice(device));
+  World* w = new World();
+  try {
+    w->device = device;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+    cudaStream_t s = w->stream;
+    w->P = P; w->rank_lo = lo; w->rank_hi = hi; w->gl = gl;
+    w->n_global = n; w->m_global = nnz / 2; w->delta_max = dmax;
+
+    DBuf<i64> goff;
+    goff.upload(h_off, n + 1, s);
+    DBuf<i32> gcol;
+    gcol.alloc(std::max<i64>(nnz, 1), s);
+    {
+      const i64 CH = (i64)1 << 26;
+      DBuf<i64> tmp;
+      tmp.alloc(std::min<i64>(std::max<i64>(nnz, 1), CH), s);
+      for (i64 b = 0; b < nnz; b += CH) {
+        const i64 k = std::min(CH, nnz - b);
+        CUDA_CHECK(cudaMemcpyAsync(tmp.p, h_col + b, sizeof(i64) * k, cudaMemcpyHostToDevice, s));
+        k_i64_to_i32<<<G(k), 256, 0, s>>>(tmp.p, gcol.p + b, k);
+        count_launch();
+      }
+    }
+    DBuf<i32> owner, owned_lid, lid_of;
+    owner.upload(owner_v.data(), n, s);
+    owned_lid.upload(owned_lid_h.data(), n, s);
+    lid_of.alloc(std::max<i64>(n, 1), s);
+    launch_fill_i32(lid_of.p, n, -1, s);
+    DBuf<uint8_t> cls, flag;
+    cls.alloc(std::max<i64>(n, 1), s);
+    cls.zero(s);
+    flag.alloc(std::max<i64>(n, 1), s);
+    DBuf<i64> cnt;
+    cnt.alloc(4, s);
+    DBuf<unsigned long long> ecount;
+    ecount.alloc(2, s);
+
+    std::vector<RankTmp> tmps((size_t)(hi - lo));
+    auto count_of = [&](const i64* dptr) {
+      i64 h = 0;
+      CUDA_CHECK(cudaMemcpyAsync(&h, dptr, sizeof(i64), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      return h;
+    };
+    for (i32 r = lo; r < hi; r++) {
+      RankTmp& T = tmps[(size_t)(r - lo)];
+      T.m.rank = r;
+      T.lgids.alloc(std::max<i64>(n, 1), s);
+      // owned (ascending gid)
+      k_flag_eq_i32<<<G(n), 256, 0, s>>>(owner.p, n, r, flag.p);
+      count_launch();
+      select_flagged(flag.p, n, T.lgids.p, cnt.p, s);
+      const i64 oc = count_of(cnt.p);
+      k_assign<<<G(oc), 256, 0, s>>>(T.lgids.p, oc, 0, 1, lid_of.p, cls.p);
+      count_launch();
+      // layer 1 = neighbours of owned not owned (ascending gid)
+      k_mark_nbrs<<<GW(oc), 256, 0, s>>>(T.lgids.p, oc, goff.p, gcol.p, cls.p, 2);
+      count_launch();
+      k_flag_eq_u8<<<G(n), 256, 0, s>>>(cls.p, n, 2, flag.p);
+      count_launch();
+      select_flagged(flag.p, n, T.lgids.p + oc, cnt.p, s);
+      const i64 l1 = count_of(cnt.p);
+      k_assign<<<G(l1), 256, 0, s>>>(T.lgids.p + oc, l1, (i32)oc, 2, lid_of.p, cls.p);
+      count_launch();
+      i64 l2 = 0;
+      if (gl == 2) {
+        k_mark_nbrs<<<GW(l1), 256, 0, s>>>(T.lgids.p + oc, l1, goff.p, gcol.p, cls.p, 3);
+        count_launch();
+        k_flag_eq_u8<<<G(n), 256, 0, s>>>(cls.p, n, 3, flag.p);
+        count_launch();
+        select_flagged(flag.p, n, T.lgids.p + oc + l1, cnt.p, s);
+        l2 = count_of(cnt.p);
+        k_assign<<<G(l2), 256, 0, s>>>(T.lgids.p + oc + l1, l2, (i32)(oc + l1), 3, lid_of.p, cls.p);
+        count_launch();
+      }
+      const i64 nl = oc + l1 + l2;
+      T.m.owned = oc; T.m.ghost = l1 + l2; T.m.l1 = l1;
+      // rows
+      DBuf<i64> len;
+      len.alloc(nl + 1, s);
+      k_rowlen<<<GW(nl), 256, 0, s>>>(T.lgids.p, nl, oc, l1, gl, goff.p, gcol.p, cls.p, len.p);
+      count_launch();
+      CUDA_CHECK(cudaMemsetAsync(len.p + nl, 0, sizeof(i64), s));
+      T.lrow.alloc(nl + 1, s);
+      exclusive_scan_i64(len.p, T.lrow.p, nl + 1, s);
+      const i64 lnnz = count_of(T.lrow.p + nl);
+      T.m.nnz = lnnz;
+      T.lcol.alloc(std::max<i64>(lnnz, 1), s);
+      k_fill<<<GW(nl), 256, 0, s>>>(T.lgids.p, nl, oc, l1, gl, goff.p, gcol.p, cls.p, lid_of.p, T.lrow.p, T.lcol.p);
+      count_launch();
+      // boundary sets and edge counts
+      DBuf<uint8_t> b1f, b2f;
+      b1f.alloc(oc + 1, s);
+      b1f.zero(s);
+      b2f.alloc(oc + 1, s);
+      ecount.zero(s);
+      k_bound1<<<G(nl), 256, 0, s>>>(T.lrow.p, T.lcol.p, nl, oc, b1f.p, ecount.p);
+      count_launch();
+      k_bound2<<<G(oc), 256, 0, s>>>(T.lrow.p, T.lcol.p, oc, b1f.p, b2f.p);
+      count_launch();
+      T.b1.alloc(oc + 1, s);
+      T.b2.alloc(oc + 1, s);
+      select_flagged(b1f.p, oc, T.b1.p, cnt.p + 1, s);
+      select_flagged(b2f.p, oc, T.b2.p, cnt.p + 2, s);
+      i64 hc[4];
+      unsigned long long he[2];
+      CUDA_CHECK(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaMemcpyAsync(he, ecount.p, sizeof(he), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      T.m.nb1 = oc > 0 ? hc[1] : 0;
+      T.m.nb2 = oc > 0 ? hc[2] : 0;
+      T.m.e_local = (i64)he[0] / 2;
+      T.m.e_ghost = (i64)he[1] / 2;
+      // gids, global degrees, ghost owners
+      T.gids.alloc(nl + 1, s);
+      T.deg.alloc(nl + 1, s);
+      T.ghost_owner.alloc(T.m.ghost + 1, s);
+      k_local_meta<<<G(nl), 256, 0, s>>>(T.lgids.p, nl, oc, goff.p, owner.p, T.gids.p, T.deg.p, T.ghost_owner.p);
+      count_launch();
+      k_reset<<<G(nl), 256, 0, s>>>(T.lgids.p, nl, lid_of.p, cls.p);
+      count_launch();
+    }
+
+    // ---- concatenate (block-diagonal local graphs)
+    i64 NL = 0, NNZ = 0, NG = 0, NB1 = 0, NB2 = 0;
+    for (auto& T : tmps) {
+      T.m.lid_off = NL; T.m.nnz_off = NNZ; T.m.ghost_off = NG; T.m.b1_off = NB1; T.m.b2_off = NB2;
+      NL += T.m.owned + T.m.ghost;
+      NNZ += T.m.nnz;
+      NG += T.m.ghost;
+      NB1 += T.m.nb1;
+      NB2 += T.m.nb2;
+    }
+    CHROMA_REQUIRE(NL < INT32_MAX, CHROMA_EVALUE, "local vertex count exceeds int32");
+    w->NL = NL; w->NNZ = NNZ; w->NGHOST = NG; w->NB1 = NB1; w->NB2 = NB2;
+    w->g.device = device; w->g.stream = s; w->g.n = NL; w->g.nnz = NNZ;
+    w->g.rowptr.alloc(NL + 1, s);
+    w->g.col.alloc(std::max<i64>(NNZ, 1), s);
+    w->gids.alloc(NL + 1, s);
+    w->deg.alloc(NL + 1, s);
+    w->colors.alloc(NL + 1, s);
+    w->colors.zero(s);
+    w->ghost_owner.alloc(NG + 1, s);
+    w->ghosts.alloc(NG + 1, s);
+    w->b1.alloc(NB1 + 1, s);
+    w->b2.alloc(NB2 + 1, s);
+    w->owned_flag.alloc(NL + 1, s);
+    w->owned_flag.zero(s);
+    w->rank_of.alloc(NL + 1, s);
+    for (auto& T : tmps) {
+      const RankMeta& m = T.m;
+      const i64 nl = m.owned + m.ghost;
+      k_shift_i64<<<G(nl), 256, 0, s>>>(T.lrow.p, w->g.rowptr.p + m.lid_off, nl, m.nnz_off);
+      k_shift_i32<<<G(m.nnz), 256, 0, s>>>(T.lcol.p, w->g.col.p + m.nnz_off, m.nnz, (i32)m.lid_off);
+      CUDA_CHECK(cudaMemcpyAsync(w->gids.p + m.lid_off, T.gids.p, sizeof(i64) * nl, cudaMemcpyDeviceToDevice, s));
+      CUDA_CHECK(cudaMemcpyAsync(w->deg.p + m.lid_off, T.deg.p, sizeof(i32) * nl, cudaMemcpyDeviceToDevice, s));
+      if (m.ghost)
+        CUDA_CHECK(cudaMemcpyAsync(w->ghost_owner.p + m.ghost_off, T.ghost_owner.p, sizeof(i32) * m.ghost,
+                                   cudaMemcpyDeviceToDevice, s));
+      k_ghost_lids<<<G(m.ghost), 256, 0, s>>>(w->ghosts.p + m.ghost_off, m.ghost, (i32)(m.lid_off + m.owned));
+      k_shift_i32<<<G(m.nb1), 256, 0, s>>>(T.b1.p, w->b1.p + m.b1_off, m.nb1, (i32)m.lid_off);
+      k_shift_i32<<<G(m.nb2), 256, 0, s>>>(T.b2.p, w->b2.p + m.b2_off, m.nb2, (i32)m.lid_off);
+      k_set_range_u8<<<G(m.owned), 256, 0, s>>>(w->owned_flag.p, m.lid_off, m.lid_off + m.owned, 1);
+      k_set_range_i32<<<G(nl), 256, 0, s>>>(w->rank_of.p, m.lid_off, m.lid_off + nl, m.rank - lo);
+      count_launch(8);
+      w->ranks.push_back(m);
+    }
+    CUDA_CHECK(cudaMemcpyAsync(w->g.rowptr.p + NL, &NNZ, sizeof(i64), cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    tmps.clear();
+
+    // ---- local routing (virtual ranks: every route has both ends in this process)
+    if (w->all_local() && NG > 0) {
+      std::vector<i64> lid_off_h((size_t)P);
+      for (auto& m : w->ranks) lid_off_h[(size_t)m.rank] = m.lid_off;
+      DBuf<i64> rank_off;
+      rank_off.upload(lid_off_h.data(), P, s);
+      DBuf<i32> src, dst, pair;
+      src.alloc(NG, s);
+      dst.alloc(NG, s);
+      pair.alloc(NG, s);
+      for (auto& m : w->ranks) {
+        k_routes<<<G(m.ghost), 256, 0, s>>>(w->gids.p, w->ghost_owner.p + m.ghost_off, m.lid_off + m.owned,
+                                             m.ghost, owned_lid.p, rank_off.p, m.rank, P,
+                                             src.p + m.ghost_off, dst.p + m.ghost_off, pair.p + m.ghost_off);
+        count_launch();
+      }
+      auto zs = thrust::make_zip_iterator(thrust::make_tuple(thrust::device_pointer_cast(dst.p),
+                                                             thrust::device_pointer_cast(pair.p)));
+      thrust::stable_sort_by_key(thrust::cuda::par.on(s), thrust::device_pointer_cast(src.p),
+                                 thrust::device_pointer_cast(src.p) + NG, zs);
+      count_launch();
+      DBuf<uint8_t> head;
+      head.alloc(NG, s);
+      k_route_heads<<<G(NG), 256, 0, s>>>(src.p, NG, head.p);
+      count_launch();
+      DBuf<i32> hpos;
+      hpos.alloc(NG, s);
+      select_flagged(head.p, NG, hpos.p, cnt.p, s);
+      const i64 nr = count_of(cnt.p);
+      w->nrouted = nr;
+      w->st_off.alloc(nr + 1, s);
+      k_route_off<<<G(nr + 1), 256, 0, s>>>(hpos.p, cnt.p, NG, w->st_off.p);
+      w->routed.alloc(nr, s);
+      k_gather_i32<<<G(nr), 256, 0, s>>>(src.p, hpos.p, cnt.p, w->routed.p);
+      count_launch(2);
+      w->st_dst = std::move(dst);
+      w->st_pair = std::move(pair);
+      w->last_sent.alloc(nr, s);
+      w->pair_cnt.alloc((i64)P * P, s);
+      w->pair_cnt.zero(s);
+    } else {
+      w->pair_cnt.alloc((i64)P * P, s);
+      w->pair_cnt.zero(s);
+    }
+    w->stats.alloc(3 + P, s);
+    w->changed.alloc(NL + 1, s);
+    world_reset_exchange(*w);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    CUDA_CHECK(cudaGetLastError());
+  } catch (...) {
+    world_destroy(w);
+    throw;
+  }
+  return w;
+}
+
+void world_destroy(World* w) {
+  if (!w) return;
+  cudaSetDevice(w->device);
+  cudaStream_t s = w->stream;
+  if (s) cudaStreamSynchronize(s);
+#ifdef CHROMA_WITH_NCCL
+  if (w->comm) ncclCommDestroy(w->comm);
+#endif
+  delete w;
+  if (s) cudaStreamDestroy(s);
+}
+
+void world_reset_exchange(World& w) {
+  if (w.nrouted) launch_fill_i32(w.last_sent.p, w.nrouted, NEVER_SENT, w.stream);
+  if (w.nrouted_remote) launch_fill_i32(w.last_sent_remote.p, w.nrouted_remote, NEVER_SENT, w.stream);
+}
+
+void world_exchange_local(World& w, bool changed_only, bool write_all) {
+  launch_exchange_local(w.routed.p, w.nrouted, w.st_off.p, w.st_dst.p, w.st_pair.p, w.colors.p,
+                        w.last_sent.p, changed_only, write_all, w.pair_cnt.p, w.stream);
+}
+
+}  // namespace chroma

@@ -1,0 +1,96 @@
+// Device-resident world: the local graphs of the ranks held by this process,
+// concatenated into one block-diagonal CSR (each rank's local ids shifted by its
+// lid offset), plus the halo routing and the protocol scratch.
+#pragma once
+#include <vector>
+
+#include "kernels.cuh"
+
+#ifdef CHROMA_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace chroma {
+
+struct RankMeta {
+  int rank = 0;
+  i64 lid_off = 0, owned = 0, ghost = 0, l1 = 0;
+  i64 nnz_off = 0, nnz = 0, e_local = 0, e_ghost = 0;
+  i64 b1_off = 0, nb1 = 0, b2_off = 0, nb2 = 0, ghost_off = 0;
+};
+
+struct Csr {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  i64 n = 0, nnz = 0;
+  DBuf<i64> rowptr;
+  DBuf<i32> col;
+};
+
+// Colouring scratch shared by every entry point that colours a CSR.
+struct ColorScratch {
+  DBuf<i32> wl, val, old, prop, pend2;
+  DBuf<i64> nwl, np2;
+  DBuf<uint8_t> flags, in_round;
+  DBuf<unsigned long long> ticket;
+};
+
+struct World {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  i32 P = 1, rank_lo = 0, rank_hi = 1, gl = 1;
+  i64 n_global = 0, m_global = 0, delta_max = 0;
+  std::vector<RankMeta> ranks;
+  i64 NL = 0, NNZ = 0, NGHOST = 0, NB1 = 0, NB2 = 0;
+  Csr g;                       // concatenated local graphs
+  DBuf<i64> gids;
+  DBuf<i32> deg;               // global degree of every local vertex (loser rule)
+  DBuf<i32> colors;
+  DBuf<i32> ghost_owner;       // per ghost slot, concatenated
+  DBuf<i32> ghosts;            // ghost lids (D1 detection rows)
+  DBuf<i32> b1, b2;            // boundary lids
+  DBuf<uint8_t> owned_flag;
+  DBuf<i32> rank_of;           // local rank index of every lid (for per-rank counts)
+  // halo routes whose endpoints are both local (virtual ranks)
+  i64 nrouted = 0;
+  DBuf<i32> routed, st_dst, st_pair, last_sent;
+  DBuf<i64> st_off;
+  DBuf<unsigned long long> pair_cnt;
+  // halo routes to other processes (NCCL)
+  bool connected = false;
+  i32 my_rank = 0;
+  std::vector<i64> send_cnt, recv_cnt, send_off, recv_off;
+  DBuf<i32> send_lids, send_peer, recv_lids, sendbuf, recvbuf;
+  i64 nsend = 0, nrecv = 0;
+  i64 nrouted_remote = 0;
+  DBuf<i32> routed_remote, last_sent_remote;
+  DBuf<uint8_t> changed;       // per local lid
+#ifdef CHROMA_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  // protocol scratch
+  ColorScratch cs;
+  DetectScratch det;
+  DBuf<unsigned long long> stats;  // [0] conflicts [1] bytes [2] msgs [3..3+P) recolored
+  DBuf<i32> deg_override;
+
+  bool all_local() const { return rank_lo == 0 && rank_hi == P; }
+  const RankMeta& meta(int rank) const {
+    CHROMA_REQUIRE(rank >= rank_lo && rank < rank_hi, CHROMA_EVALUE, "rank not held by this world");
+    return ranks[rank - rank_lo];
+  }
+};
+
+World* world_create(i64 n, const i64* off, const i64* col, i32 P, const i32* owner, i32 gl, i32 lo,
+                    i32 hi, int device);
+void world_destroy(World* w);
+void world_reset_exchange(World& w);
+void world_exchange_local(World& w, bool changed_only, bool write_all);
+
+// Colour the worklist of a CSR (absolute vertex ids).  `wl_sorted_unique` skips the
+// device sort/dedupe for protocol worklists that are produced in order.
+void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32* wl_dev,
+               const i64* nwl_dev, i64 nwl_max, bool wl_sorted_unique, int dist, bool partial,
+               int algo, bool colors_nonneg, ColorScratch& S, cudaStream_t s);
+
+}  // namespace chroma

@@ -1,0 +1,135 @@
+"""One rank per GPU process: the multi-GPU form of the reference's simulated world.
+
+Every process (launched by torchrun, one per B200) builds only its own rank's local
+graph on its GPU (same layout as runtime.build_local_graphs), agrees on the static
+halo routing with its peers once (host logic below, over torch.distributed), and then
+runs the whole round loop inside libchroma_b200 with its own NCCL communicator:
+pack -> grouped ncclSend/ncclRecv over NVLink -> unpack, and one ncclAllReduce of
+[conflicts, bytes, messages, recolored_per_rank...] per round (chroma/protocol.py:
+288-329; chroma/runtime.py:271-316).
+
+torch.distributed is plumbing only: it carries the NCCL unique id and the one-time
+routing lists.  The per-round traffic never touches Python.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .graph import stats as graph_stats
+from .runtime import LocalGraph, ProtocolError, WorldHandle
+
+__all__ = ["build_routing", "DistWorld", "torch_alltoallv"]
+
+
+def build_routing(gids: np.ndarray, owned_count: int, ghost_owner: np.ndarray, num_ranks: int, rank: int,
+                  alltoallv):
+    """Static halo routing of one rank.
+
+    recv side: this rank's ghost slots grouped by owner, slot order kept (the owner
+    sends in exactly that order); send side: the owned local ids every peer asked for.
+    `alltoallv(list_of_int64_arrays_per_peer) -> list_of_received_arrays` is the only
+    communication.  Returns (send_counts, send_lids, recv_counts, recv_lids), local ids.
+    """
+    gids = np.asarray(gids, dtype=np.int64)
+    go = np.asarray(ghost_owner, dtype=np.int64)
+    slots = np.argsort(go, kind="stable")
+    recv_counts = np.bincount(go, minlength=num_ranks).astype(np.int64)
+    recv_lids = (owned_count + slots).astype(np.int64)
+    req = gids[owned_count:][slots]
+    bounds = np.concatenate([[0], np.cumsum(recv_counts)])
+    outgoing = [req[bounds[p]: bounds[p + 1]] for p in range(num_ranks)]
+    if recv_counts[rank]:
+        raise ProtocolError(f"rank {rank} holds a ghost of its own vertex")
+    incoming = alltoallv(outgoing)
+    owned = gids[:owned_count]
+    send_counts = np.array([len(x) for x in incoming], dtype=np.int64)
+    asked = np.concatenate(incoming) if len(incoming) else np.empty(0, np.int64)
+    lids = np.searchsorted(owned, asked)
+    ok = (lids < owned_count) & (owned[np.minimum(lids, max(owned_count - 1, 0))] == asked) if owned_count \
+        else np.zeros(asked.shape, bool)
+    if not np.all(ok):
+        bad = asked[~ok][0]
+        raise ProtocolError(f"rank {rank} received unknown gid {int(bad)}")
+    return send_counts, lids.astype(np.int64), recv_counts, recv_lids
+
+
+def torch_alltoallv(group=None, device=None):
+    """alltoallv over torch.distributed (gloo on CPU tensors, nccl on CUDA tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    def run(outgoing):
+        dev = device if device is not None else "cpu"
+        P = len(outgoing)
+        send_counts = torch.tensor([len(x) for x in outgoing], dtype=torch.int64, device=dev)
+        recv_counts = torch.empty(P, dtype=torch.int64, device=dev)
+        dist.all_to_all_single(recv_counts, send_counts, group=group)
+        rc = recv_counts.cpu().tolist()
+        send = torch.from_numpy(np.concatenate(outgoing).astype(np.int64) if sum(len(x) for x in outgoing)
+                                else np.zeros(0, np.int64)).to(dev)
+        recv = torch.empty(int(sum(rc)), dtype=torch.int64, device=dev)
+        dist.all_to_all_single(recv, send, output_split_sizes=rc,
+                               input_split_sizes=[len(x) for x in outgoing], group=group)
+        r = recv.cpu().numpy()
+        b = np.concatenate([[0], np.cumsum(rc)]).astype(np.int64)
+        return [r[b[p]: b[p + 1]] for p in range(P)]
+
+    return run
+
+
+class DistWorld:
+    """This process's rank of a num_ranks-way partition, on its own GPU."""
+
+    def __init__(self, g, pm, ghost_layers: int, rank: int | None = None, group=None, device: int | None = None):
+        import torch
+        import torch.distributed as dist
+        if ghost_layers not in (1, 2):
+            raise ValueError("ghost_layers must be 1 or 2")
+        pm.validate()
+        if len(pm.owner) != g.num_vertices:
+            raise ValueError("partition size does not match graph")
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.num_ranks = pm.num_ranks
+        if dist.get_world_size(group) != self.num_ranks:
+            raise ValueError("one process per rank is required")
+        self.device = torch.cuda.current_device() if device is None else device
+        _lib.set_device(self.device)
+        self.ghost_layers = ghost_layers
+        self.partition = pm
+        self.num_global_vertices = g.num_vertices
+        self.source_stats = graph_stats(g)
+        self.handle = WorldHandle(g, pm, ghost_layers, self.rank, self.rank + 1, self.device)
+        self.local_graph = LocalGraph(self.handle, self.rank, ghost_layers)
+        self.local_graphs = [self.local_graph]
+        self.total_bytes = 0
+        self.total_messages = 0
+        lg = self.local_graph
+        routing = build_routing(lg.gids, lg.owned_count, lg.ghost_owner, self.num_ranks, self.rank,
+                                torch_alltoallv(group, device=f"cuda:{self.device}"))
+        idbuf = (C.c_char * 128)()
+        if self.rank == 0:
+            _lib.check(_lib.lib().chroma_nccl_unique_id(idbuf))
+        obj = [bytes(idbuf) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        idbuf = (C.c_char * 128).from_buffer_copy(obj[0])
+        sc, sl, rc, rl = (_lib.i64(x) for x in routing)
+        _lib.check(_lib.lib().chroma_world_connect(self.handle.h, idbuf, self.num_ranks, self.rank,
+                                                   _lib.ptr(sc), _lib.ptr(sl), _lib.ptr(rc), _lib.ptr(rl)),
+                   "chroma_world_connect")
+        self.halo_send = int(sc.sum())
+        self.halo_recv = int(rc.sum())
+
+    def output_length(self) -> int:
+        return self.local_graph.owned_count
+
+    def owned_range(self):
+        g = self.local_graph.gids
+        return g[: self.local_graph.owned_count]
+
+    def reset_exchange_state(self) -> None:
+        self.total_bytes = 0
+        self.total_messages = 0
+        _lib.check(_lib.lib().chroma_world_reset_exchange(self.handle.h))
