@@ -164,6 +164,11 @@ int chroma_run_distributed(chroma_world* w, int mode, int recolor_degrees, int a
  * (for zero-copy verification/bench). */
 int chroma_world_colors_device(chroma_world* w, int32_t rank, int32_t** dev_ptr, int64_t* lid_offset);
 
+/* CUDA-event times of the last chroma_run_distributed on this world, seconds:
+ * out[0] whole call on the device stream, out[1] colouring kernel only (summed over
+ * rounds), out[2] colour phase, out[3] exchange phase, out[4] detect phase. */
+int chroma_world_last_timing(chroma_world* w, double* out5);
+
 /* Number of kernels this library launched on `w` (or globally if w is NULL). */
 int64_t chroma_launch_count(void);
 

@@ -66,6 +66,7 @@ def lib():
         "chroma_world_detect": (I, [P, i32, P, P, I, I, I, PI64]),
         "chroma_run_distributed": (I, [P, I, I, I, I, P, P, P, i64, PI64, u32]),
         "chroma_world_colors_device": (I, [P, i32, C.POINTER(P), PI64]),
+        "chroma_world_last_timing": (I, [P, P]),
         "chroma_launch_count": (i64, []),
     }
     for name, (res, args) in sig.items():
@@ -83,7 +84,8 @@ EXPORTS = ("chroma_last_error", "chroma_version", "chroma_device_count", "chroma
            "chroma_world_rank_info", "chroma_world_rank_arrays", "chroma_nccl_unique_id",
            "chroma_world_connect", "chroma_world_global_degrees", "chroma_world_reset_exchange",
            "chroma_world_exchange", "chroma_world_color", "chroma_world_detect",
-           "chroma_run_distributed", "chroma_world_colors_device", "chroma_launch_count")
+           "chroma_run_distributed", "chroma_world_colors_device", "chroma_world_last_timing",
+           "chroma_launch_count")
 
 
 def check(status: int, what: str = "") -> None:

@@ -528,6 +528,17 @@ int chroma_run_distributed(chroma_world* h, int mode, int rd, int algo, int max_
   return g != CHROMA_OK ? g : st;
 }
 
+int chroma_world_last_timing(chroma_world* h, double* out) {
+  return guarded([&] {
+    const World& w = *h->w;
+    out[0] = w.t_total;
+    out[1] = w.t_color_kernel;
+    out[2] = w.t_color;
+    out[3] = w.t_comm;
+    out[4] = w.t_detect;
+  });
+}
+
 int chroma_world_colors_device(chroma_world* h, int32_t rank, int32_t** dev_ptr, int64_t* lid_offset) {
   return guarded([&] {
     const RankMeta& m = h->w->meta(rank);

@@ -67,7 +67,8 @@ constexpr int MAX_SWEEPS = 10000;  // chroma/localcolor.py:34
 // ------------------------------------------------------------------ colouring driver
 void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32* wl_in,
                const i64* nwl_dev, i64 nwl_max, bool wl_sorted_unique, int dist, bool partial,
-               int algo, bool colors_nonneg, ColorScratch& S, cudaStream_t s) {
+               int algo, bool colors_nonneg, ColorScratch& S, cudaStream_t s, cudaEvent_t ev_k0,
+               cudaEvent_t ev_k1) {
   if (nwl_max <= 0) return;
   S.nwl.reserve(1, s);
   S.ticket.reserve(1, s);
@@ -111,7 +112,9 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     L.ticket = S.ticket.p;
     L.dist = dist;
     L.partial = partial;
+    if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
     launch_gs(L, s);
+    if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
     if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
     return;
   }
@@ -231,8 +234,10 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   w.cs.flags.reserve(w.NL + 1, s);
   const i64 nstats = 3 + w.P;
   std::vector<unsigned long long> hs((size_t)nstats);
-  cudaEvent_t ev[4];
+  cudaEvent_t ev[8];
   for (auto& e : ev) CUDA_CHECK(cudaEventCreate(&e));
+  w.t_total = w.t_color_kernel = w.t_color = w.t_comm = w.t_detect = 0;
+  CUDA_CHECK(cudaEventRecord(ev[4], s));
   int status = CHROMA_OK;
   i64 round = 0;
   DetectArgs da;
@@ -266,8 +271,9 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     k_count_recolored<<<G(w.NL), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
                                               w.stats.p);
     count_launch();
+    const bool gs_like = algo != CHROMA_ALGO_JACOBI;
     color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, w.NL, true, dist, partial,
-              algo, true, w.cs, s);
+              algo, true, w.cs, s, gs_like ? ev[6] : nullptr, gs_like ? ev[7] : nullptr);
     CUDA_CHECK(cudaEventRecord(ev[1], s));
     // exchange: every ghost takes its owner's colour; accounting is changed-only
     if (w.nrouted) {
@@ -285,7 +291,9 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     CUDA_CHECK(cudaMemcpyAsync(hs.data(), w.stats.p, sizeof(unsigned long long) * nstats,
                                cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-    float t01 = 0, t12 = 0, t23 = 0;
+    float t01 = 0, t12 = 0, t23 = 0, tk = 0;
+    if (gs_like && w.NL > 0) cudaEventElapsedTime(&tk, ev[6], ev[7]);
+    w.t_color_kernel += tk * 1e-3;
     cudaEventElapsedTime(&t01, ev[0], ev[1]);
     cudaEventElapsedTime(&t12, ev[1], ev[2]);
     cudaEventElapsedTime(&t23, ev[2], ev[3]);
@@ -297,11 +305,13 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     R.time_color_s = t01 * 1e-3;
     R.time_comm_s = t12 * 1e-3;
     R.time_detect_s = t23 * 1e-3;
+    w.t_color += R.time_color_s;
+    w.t_comm += R.time_comm_s;
+    w.t_detect += R.time_detect_s;
     for (i32 r = 0; r < w.P; r++) recolored[round * w.P + r] = (i64)hs[(size_t)(3 + r)];
     round++;
     if (hs[0] == 0) break;
   }
-  for (auto& e : ev) cudaEventDestroy(e);
   *n_reports = round;
   if (status == CHROMA_OK && colors_out) {
     if (w.all_local()) {
@@ -322,8 +332,15 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
       CUDA_CHECK(cudaMemcpyAsync(colors_out, w.colors.p + m.lid_off, sizeof(i32) * m.owned,
                                  out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     }
-    CUDA_CHECK(cudaStreamSynchronize(s));
   }
+  CUDA_CHECK(cudaEventRecord(ev[5], s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  {
+    float tt = 0;
+    cudaEventElapsedTime(&tt, ev[4], ev[5]);
+    w.t_total = tt * 1e-3;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
   return status;
 }
 

@@ -73,6 +73,8 @@ struct World {
   DetectScratch det;
   DBuf<unsigned long long> stats;  // [0] conflicts [1] bytes [2] msgs [3..3+P) recolored
   DBuf<i32> deg_override;
+  // device-side timing of the last run_distributed (CUDA events on `stream`)
+  double t_total = 0, t_color_kernel = 0, t_color = 0, t_comm = 0, t_detect = 0;
 
   bool all_local() const { return rank_lo == 0 && rank_hi == P; }
   const RankMeta& meta(int rank) const {
@@ -91,6 +93,7 @@ void world_exchange_local(World& w, bool changed_only, bool write_all);
 // device sort/dedupe for protocol worklists that are produced in order.
 void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32* wl_dev,
                const i64* nwl_dev, i64 nwl_max, bool wl_sorted_unique, int dist, bool partial,
-               int algo, bool colors_nonneg, ColorScratch& S, cudaStream_t s);
+               int algo, bool colors_nonneg, ColorScratch& S, cudaStream_t s,
+               cudaEvent_t ev_k0 = nullptr, cudaEvent_t ev_k1 = nullptr);
 
 }  // namespace chroma
