@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""Benchmark: distributed speculate-and-iterate colouring on B200 (BASELINE.json metric).
+
+Workload (configs[1], "C2"): D1-2GL colouring of the 3-D 27-point stencil mesh 128^3
+(2,097,152 vertices, 26,822,908 undirected edges), partition_block over P = N ranks,
+one rank per GPU, deterministic mode (bit-exact with the reference).  One step = one
+full run_distributed (every round: colour, halo exchange over NVLink, detection,
+allreduce) on the device-resident world.
+
+    python bench.py [--gpus N --steps K --warmup W]            # our B200 path
+    python bench.py --impl reference [...]                      # reference arm (CPU)
+    torchrun --nproc-per-node N bench.py --gpus N ...           # N > 1
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "coloring edges/s (D1-2GL, 27-pt stencil 128^3)"
+UNIT = "edges/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--L", type=int, default=128, help="stencil edge length (128 = BASELINE config)")
+    ap.add_argument("--algorithm", default="gauss-seidel", choices=["gauss-seidel", "free", "jacobi"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def c2_graph(L: int, device=None):
+    from paper_2107_00075_b200 import graph as G
+    return G.gen_stencil27(L, device=device)
+
+
+def round0_bytes(n_owned: int, nnz_owned: int, touched: int) -> int:
+    """Algorithmic bytes of one round-0 colouring launch: colour write,
+    row pointers (int64 pair per row), int32 column indices, distinct colours read."""
+    return 4 * n_owned + 8 * (n_owned + 1) + 4 * nnz_owned + 4 * touched
+
+
+def cpu_baseline(L: int, P: int, budget_s: float = 30.0) -> dict:
+    """The C oracle (port of the reference path) on the host, single thread."""
+    import oracle
+    from paper_2107_00075_b200 import partition as PT
+    g = c2_graph(L)
+    pm = PT.partition_block(g, P)
+    w = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, 2)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        w.run("d1-2gl", False, True)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el > budget_s / 3 or reps >= 3:
+            break
+    sec = el / reps
+    m = len(g.col_indices) // 2
+    return {"value": m / sec, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle run_distributed (D1-2GL deterministic) on the full 27-pt {L}^3 mesh, "
+                      f"P={P}, {reps} rep(s), {sec:.3f} s/step, 1 of {os.cpu_count()} cores"}
+
+
+def run_reference(args):
+    """Reference arm: the CPU port of the reference path (oracle/), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2107_00075_b200 import partition as PT
+    P = args.gpus
+    g = c2_graph(args.L)
+    pm = PT.partition_block(g, P)
+    w = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, 2)
+    for _ in range(args.warmup):
+        w.run("d1-2gl", False, True)
+    t = []
+    colors = None
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        colors, reps = w.run("d1-2gl", False, True)
+        t.append(time.perf_counter() - t0)
+    m = len(g.col_indices) // 2
+    T = sum(t)
+    val = m * args.steps / T
+    ncol = int(len(np.unique(colors[colors > 0])))
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": P, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"C2: D1-2GL 27-point stencil {args.L}^3, partition_block P={P}, deterministic",
+                       "n": g.num_vertices, "m": m, "rounds": len(reps), "colors": ncol},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"oracle/ C port of the reference path, full workload each step, "
+                                       f"1 of {os.cpu_count()} cores"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2107_00075_b200 import launch_count
+    from paper_2107_00075_b200 import partition as PT
+    from paper_2107_00075_b200 import protocol as R
+    from paper_2107_00075_b200 import runtime as RT
+    from paper_2107_00075_b200 import verify as V
+    from paper_2107_00075_b200 import _lib
+
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = world_size
+    if N != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={N}")
+    torch.cuda.set_device(local)
+    _lib.set_device(local)
+    if N > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    def barrier():
+        if N > 1:
+            dist.barrier()
+
+    def allmax(x: float) -> float:
+        if N == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    g = c2_graph(args.L, device=f"cuda:{local}")
+    m = len(g.col_indices) // 2
+    pm = PT.partition_block(g, N)
+    cfg = R.AlgorithmConfig(mode=R.Mode.D1_2GL, deterministic=args.algorithm == "gauss-seidel",
+                            algorithm=None if args.algorithm == "gauss-seidel" else args.algorithm)
+
+    def make_world():
+        if N == 1:
+            return RT.build_local_graphs(g, pm, 2)
+        from paper_2107_00075_b200.dist import DistWorld
+        return DistWorld(g, pm, 2)
+
+    world = make_world()
+    lg = world.local_graphs[0] if N == 1 else world.local_graph
+    for _ in range(args.warmup):
+        R.run_distributed(world, cfg)
+
+    import ctypes as C
+    tbuf = (C.c_double * 5)()
+    barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local) if rank == 0 else None
+    l0 = launch_count()
+    per = []
+    kern = []
+    rounds = 0
+    colors = None
+    for _ in range(args.steps):
+        barrier()
+        colors, reports = R.run_distributed(world, cfg)
+        _lib.check(_lib.lib().chroma_world_last_timing(world.handle.h, tbuf))
+        per.append(tbuf[0])
+        kern.append(tbuf[1])
+        rounds = len(reports)
+    torch.cuda.synchronize()
+    barrier()
+    launches = launch_count() - l0
+    clocks = clk.stop() if clk else None
+    T = allmax(sum(per))
+    TK = allmax(sum(kern))
+    value = m * args.steps / T
+    # ---- colour count and properness (global, after timing)
+    if N == 1:
+        gcol = colors
+    else:
+        own = torch.from_numpy(colors.astype(np.int32)).cuda()
+        sizes = [None] * N
+        dist.all_gather_object(sizes, int(own.numel()))
+        bufs = [torch.empty(s, dtype=torch.int32, device=own.device) for s in sizes]
+        dist.all_gather(bufs, own)
+        gcol = torch.cat(bufs).cpu().numpy()  # partition_block: owned ranges are contiguous in gid order
+    ncol, _ = V.color_stats(gcol) if rank == 0 else (None, None)
+    nviol = V.count_violations(g, gcol, "d1") if rank == 0 else None
+    # ---- roofline of the dominant kernel (GS colouring, round 0 bytes)
+    n_o = lg.owned_count
+    nnz_o = int(lg.row_offsets[n_o]) if N > 1 else len(g.col_indices)
+    touched = lg.num_local if N > 1 else g.num_vertices
+    B = round0_bytes(n_o, nnz_o, touched)
+    kernel_s = TK / args.steps
+    peak, peak_kind = peaks()
+    achieved = B / kernel_s / 1e9
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        off_p = torch.from_numpy(np.ascontiguousarray(g.row_offsets, dtype=np.int64)).pin_memory()
+        col_p = torch.from_numpy(np.ascontiguousarray(g.col_indices, dtype=np.int64)).pin_memory()
+        own_p = torch.from_numpy(np.ascontiguousarray(pm.owner, dtype=np.int32)).pin_memory()
+        from paper_2107_00075_b200.graph import Graph
+        hg = Graph(g.num_vertices, off_p.numpy(), col_p.numpy())
+        hpm = PT.PartitionMap(own_p.numpy(), N)
+        et = []
+        for it in range(max(1, min(args.steps, 3)) + 1):
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if N == 1:
+                wv = RT.build_local_graphs(hg, hpm, 2)
+            else:
+                from paper_2107_00075_b200.dist import DistWorld
+                wv = DistWorld(hg, hpm, 2)
+            out, _ = R.run_distributed(wv, cfg)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            del wv
+            if it > 0:
+                et.append(el)
+        te = allmax(sum(et) / len(et))
+        e2e = {"value": m / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(off_p.numel() * 8 + col_p.numel() * 8 + own_p.numel() * 4),
+               "d2h_bytes_per_step": int(4 * (g.num_vertices if N == 1 else n_o)),
+               "timing": "host perf_counter around build_local_graphs + run_distributed (synchronous API)"}
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.L, N)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+                "data": "synthetic (27-point stencil generated on device, id = x + L(y + L z))",
+                "config": {"workload": f"C2: D1-2GL 27-point stencil {args.L}^3, partition_block P={N}, "
+                                       f"{args.algorithm}",
+                           "n": g.num_vertices, "m": m, "ghost_layers": 2, "rounds": rounds, "colors": ncol,
+                           "violations": nviol, "parallelism": f"vertex-range x{N}",
+                           "l2": f"inputs larger than L2 (int32 col {4 * len(g.col_indices) / 1e6:.0f} MB)"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None, "kernel": "gs_kernel (colouring)",
+                             "algorithmic_bytes_per_launch": B, "kernel_ms": kernel_s * 1e3,
+                             "peak_kind": peak_kind},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if N > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -26,6 +26,9 @@
 //   * vertices whose first 256 colours are all forbidden take a warp-cooperative
 //     rescan window by window (the reference's 64-colour window walk,
 //     chroma/localcolor.py:64-112, generalised).
+#include <cstdlib>
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace chroma {
@@ -34,25 +37,28 @@ namespace {
 
 constexpr int WORDS = 8;                 // 8 x 32 bits = colours 1..256 in the fast path
 constexpr int FAST_COLORS = 32 * WORDS;
-constexpr int WARPS = 8;
-constexpr int QCAP = 192;                // per-warp queue of unresolved earlier dependencies
+constexpr int WARPS = 4;
+constexpr i64 HEAVY = 64;                // forbidden sets larger than this are rescanned by the warp
+constexpr unsigned NS_MAX = 512;         // idle polling back-off cap (ns)
+constexpr int PL = 24;                   // per-lane list of pending earlier dependencies
 constexpr unsigned FULL = 0xffffffffu;
 
 struct WarpSmem {
   u32 mask[32][WORDS];
-  u32 dep[32];
+  u32 dep[32];                 // in-chunk predecessors (lane mask)
   i32 key[32];
   i32 v[32];
-  i32 pend[32];
+  i32 pcnt[32];                // earlier vertices still pending at the last scan
+  unsigned long long sent[32]; // sentinel: max (key << 32 | vertex) among them
+  i32 plist[32][PL];           // the pending ones (first PL; povf marks overflow)
+  u32 povf[32];
   i32 ccol[32];
+  i64 setsz[32];               // size of the forbidden-set walk (rescan cost)
   i64 excl[32];
   i64 rs[32];
   i64 excl2[32];
   i64 rs2[32];
   i32 own2[32];
-  i32 qx[QCAP];
-  uint8_t qj[QCAP];
-  int qlen;
 };
 
 struct GsArgs {
@@ -65,9 +71,20 @@ struct GsArgs {
   const i64* nwl;     // device scalar: worklist length
   const i32* prio;    // optional ordering key (serial_greedy with an order)
   unsigned long long* ticket;
+  unsigned long long* trace;  // optional per-chunk timestamps (CHROMA_GS_TRACE)
+  unsigned long long* vtrace; // optional per-worklist-entry commit timestamps
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ i32 key_of(const GsArgs& a, i32 x) { return a.prio ? a.prio[x] : x; }
+__device__ __forceinline__ unsigned long long pack(i32 k, i32 x) {
+  return ((unsigned long long)(u32)k << 32) | (u32)x;
+}
 
 // largest j in [0,32) with arr[j] <= e (arr nondecreasing, arr[0] <= e)
 template <typename T>
@@ -83,7 +100,7 @@ __device__ __forceinline__ void forbid(WarpSmem& sm, int j, i32 c) {
   if (c > 0 && c <= FAST_COLORS) atomicOr(&sm.mask[j][(c - 1) >> 5], 1u << ((c - 1) & 31));
 }
 
-// One forbidden-set candidate x of chunk lane j.
+// One forbidden-set candidate x of chunk lane j (phase A).
 __device__ __forceinline__ void visit(const GsArgs& a, WarpSmem& sm, int j, i32 x, i32 kfirst,
                                       bool ident_lanes, i32 vfirst) {
   i32 c = a.val[x];  // a stale L1 copy can only read PENDING; resolved below
@@ -98,25 +115,32 @@ __device__ __forceinline__ void visit(const GsArgs& a, WarpSmem& sm, int j, i32 
       atomicOr(&sm.dep[j], 1u << l);
       return;
     } else {
-      c = ld_relaxed(a.val + x);
-      if (c == PENDING) {
-        const int q = atomicAdd(&sm.qlen, 1);
-        if (q < QCAP) {
-          sm.qx[q] = x;
-          sm.qj[q] = (uint8_t)j;
-          atomicAdd(&sm.pend[j], 1);
-          return;
-        }
-        unsigned ns = 32;
-        do {  // queue overflow: wait in place
-          __nanosleep(ns);
-          ns = ns < 512 ? ns * 2 : ns;
-          c = ld_relaxed(a.val + x);
-        } while (c == PENDING);
-      }
+      // possibly a stale PENDING: the list check in phase B resolves it
+      const int k = atomicAdd(&sm.pcnt[j], 1);
+      if (k < PL) sm.plist[j][k] = x;
+      else sm.povf[j] = 1;
+      atomicMax(&sm.sent[j], pack(kx, x));
+      return;
     }
   }
   forbid(sm, j, c);
+}
+
+// Re-visit of a forbidden-set candidate once the lane's sentinel committed:
+// committed colours are folded (idempotent), earlier pending ones counted.
+__device__ __forceinline__ void revisit(const GsArgs& a, WarpSmem& sm, int j, i32 x, i32 kfirst, int& pend,
+                                        unsigned long long& best) {
+  const i32 c = ld_relaxed(a.val + x);
+  if (c == PENDING) {
+    const i32 kx = key_of(a, x);
+    if (kx < kfirst) {
+      pend++;
+      const unsigned long long p = pack(kx, x);
+      best = p > best ? p : best;
+    }
+  } else {
+    forbid(sm, j, c);
+  }
 }
 
 __device__ __forceinline__ int first_free(const u32 (&m)[WORDS]) {
@@ -126,34 +150,40 @@ __device__ __forceinline__ int first_free(const u32 (&m)[WORDS]) {
   return 0;
 }
 
+// Walk v's forbidden set: D1 N(v); D2 N(v) u N2(v); PD2 N2(v) -- split over `lanes`
+// threads starting at `first` (1 = lane-serial, 32 = warp-cooperative).
+template <int DIST, bool PARTIAL, typename F>
+__device__ __forceinline__ void walk_set(const GsArgs& a, i32 v, int first, int lanes, F&& f) {
+  const i64 rs = a.rowptr[v], re = a.rowptr[v + 1];
+  if (DIST == 1) {
+    for (i64 e = rs + first; e < re; e += lanes) f(a.col[e]);
+  } else {
+    for (i64 e = rs; e < re; e++) {
+      const i32 u = a.col[e];
+      if (!PARTIAL && first == 0) f(u);
+      const i64 us = a.rowptr[u], ue = a.rowptr[u + 1];
+      for (i64 g = us + first; g < ue; g += lanes) {
+        const i32 x = a.col[g];
+        if (x != v) f(x);
+      }
+    }
+  }
+}
+
 // Warp-cooperative colour search above the fast window, once every dependency of v
 // is committed.  Uniform across the warp.
 template <int DIST, bool PARTIAL>
 __device__ i32 slow_color(const GsArgs& a, i32 v, i32 kv, int lane) {
-  const i64 rs = a.rowptr[v], re = a.rowptr[v + 1];
   for (i32 base = FAST_COLORS + 1;; base += FAST_COLORS) {
     u32 m[WORDS];
 #pragma unroll
     for (int w = 0; w < WORDS; w++) m[w] = 0;
-    auto consider = [&](i32 x) {
+    walk_set<DIST, PARTIAL>(a, v, lane, 32, [&](i32 x) {
       i32 c = ld_relaxed(a.val + x);
       if (c == PENDING) c = (key_of(a, x) > kv && a.old) ? a.old[x] : 0;
       const i32 o = c - base;
       if (o >= 0 && o < FAST_COLORS) m[o >> 5] |= 1u << (o & 31);
-    };
-    if (DIST == 1) {
-      for (i64 e = rs + lane; e < re; e += 32) consider(a.col[e]);
-    } else {
-      for (i64 e = rs; e < re; e++) {
-        const i32 u = a.col[e];
-        if (!PARTIAL && lane == 0) consider(u);
-        const i64 us = a.rowptr[u], ue = a.rowptr[u + 1];
-        for (i64 f = us + lane; f < ue; f += 32) {
-          const i32 x = a.col[f];
-          if (x != v) consider(x);
-        }
-      }
-    }
+    });
 #pragma unroll
     for (int w = 0; w < WORDS; w++) m[w] = __reduce_or_sync(FULL, m[w]);
     const int r = first_free(m);
@@ -176,6 +206,8 @@ gs_kernel(GsArgs a) {
     if (lane == 0) t = atomicAdd(a.ticket, 1ull);
     const i64 chunk = (i64)__shfl_sync(FULL, t, 0);
     if (chunk >= nchunks) break;
+    unsigned long long t_claim = 0;
+    if (a.trace && lane == 0) t_claim = gtimer();
 
     const i64 idx = chunk * 32 + lane;
     const bool act = idx < nwl;
@@ -195,15 +227,17 @@ gs_kernel(GsArgs a) {
     sm.key[lane] = kv;
     sm.v[lane] = v;
     sm.dep[lane] = 0;
-    sm.pend[lane] = 0;
+    sm.pcnt[lane] = 0;
+    sm.sent[lane] = 0;
+    sm.povf[lane] = 0;
+    sm.setsz[lane] = DIST == 1 ? d : 0;
 #pragma unroll
     for (int w = 0; w < WORDS; w++) sm.mask[lane][w] = 0;
-    if (lane == 0) sm.qlen = 0;
     const i32 kfirst = __shfl_sync(FULL, kv, 0);
     const i32 vfirst = __shfl_sync(FULL, v, 0);
     __syncwarp();
 
-    // ---------------- phase A: fold committed colours, queue the earlier pending ones
+    // ---------------- phase A: fold committed colours, count the earlier pending ones
     if (DIST == 1) {
       for (i64 base = 0; base < total; base += 32) {
         const i64 e = base + lane;
@@ -225,6 +259,7 @@ gs_kernel(GsArgs a) {
           u = a.col[sm.rs[j] + (e - sm.excl[j])];
           us = a.rowptr[u];
           d2 = a.rowptr[u + 1] - us;
+          atomicAdd((unsigned long long*)&sm.setsz[j], (unsigned long long)(d2 + 1));
         }
         i64 incl2 = d2;
 #pragma unroll
@@ -253,17 +288,19 @@ gs_kernel(GsArgs a) {
     }
     __syncwarp();
 
+    unsigned long long t_a = 0;
+    if (a.trace && lane == 0) t_a = gtimer();
+
     // ---------------- phase B: per-lane dataflow commit
     const u32 mydep = sm.dep[lane];
-    const int qn = min(sm.qlen, QCAP);
     bool done = !act;
     u32 donemask = __ballot_sync(FULL, done);
-    unsigned ns = 32;
+    unsigned ns = 64;
     while (donemask != FULL) {
       // commit every lane whose dependencies are all satisfied; repeat while the
       // in-chunk chain keeps advancing (no global traffic in this inner loop)
       for (;;) {
-        const bool ready = !done && sm.pend[lane] == 0 && (mydep & ~donemask) == 0;
+        const bool ready = !done && sm.pcnt[lane] == 0 && (mydep & ~donemask) == 0;
         int r = 1;
         if (ready) {
           u32 m[WORDS];
@@ -275,6 +312,7 @@ gs_kernel(GsArgs a) {
           }
           r = first_free(m);
           if (r) {
+            if (a.vtrace) a.vtrace[idx] = gtimer();
             st_relaxed(a.val + v, r);
             sm.ccol[lane] = r;
             done = true;
@@ -297,30 +335,79 @@ gs_kernel(GsArgs a) {
         donemask = nd;
       }
       if (donemask == FULL) break;
-      // poll the queued earlier dependencies once
-      bool got = false;
-      for (int q = lane; q < qn; q += 32) {
-        const i32 x = sm.qx[q];
-        if (x >= 0) {
-          const i32 c = ld_relaxed(a.val + x);
-          if (c != PENDING) {
-            const int j = sm.qj[q];
-            forbid(sm, j, c);
-            sm.qx[q] = -1;
-            atomicSub(&sm.pend[j], 1);
-            got = true;
+      // poll one sentinel per waiting lane (its largest-key pending earlier vertex);
+      // adjacent lanes usually wait on adjacent vertices, so the loads coalesce
+      bool need = false;
+      if (!done && sm.pcnt[lane] > 0) need = ld_relaxed(a.val + (i32)(sm.sent[lane] & 0xffffffffu)) != PENDING;
+      if (!__any_sync(FULL, need)) {
+        __nanosleep(ns);
+        ns = ns < NS_MAX ? ns * 2 : ns;
+        continue;
+      }
+      ns = 64;
+      // listed dependencies: one batch of independent loads, keep the still-pending
+      const bool listed = need && !sm.povf[lane];
+      if (listed) {
+        const int n = sm.pcnt[lane];
+        i32 xs[PL], cs[PL];
+#pragma unroll
+        for (int k = 0; k < PL; k++) {
+          xs[k] = k < n ? sm.plist[lane][k] : 0;
+          cs[k] = k < n ? ld_relaxed(a.val + xs[k]) : 0;
+        }
+        int w = 0;
+        unsigned long long best = 0;
+#pragma unroll
+        for (int k = 0; k < PL; k++) {
+          if (k >= n) break;
+          if (cs[k] == PENDING) {
+            sm.plist[lane][w++] = xs[k];
+            const unsigned long long p = pack(key_of(a, xs[k]), xs[k]);
+            best = p > best ? p : best;
+          } else {
+            forbid(sm, lane, cs[k]);
           }
+        }
+        sm.pcnt[lane] = w;
+        sm.sent[lane] = best;
+      }
+      // overflowed lists: walk the whole set again (light lane-serially, heavy by the warp)
+      const bool walk = need && !listed;
+      const bool heavy = walk && sm.setsz[lane] > HEAVY;
+      if (walk && !heavy) {
+        int pend = 0;
+        unsigned long long best = 0;
+        walk_set<DIST, PARTIAL>(a, v, 0, 1, [&](i32 x) { revisit(a, sm, lane, x, kfirst, pend, best); });
+        sm.pcnt[lane] = pend;
+        sm.sent[lane] = best;
+      }
+      u32 hv = __ballot_sync(FULL, heavy);
+      while (hv) {
+        const int l = __ffs(hv) - 1;
+        hv &= hv - 1;
+        const i32 vl = __shfl_sync(FULL, v, l);
+        int pend = 0;
+        unsigned long long best = 0;
+        walk_set<DIST, PARTIAL>(a, vl, lane, 32, [&](i32 x) { revisit(a, sm, l, x, kfirst, pend, best); });
+        pend = __reduce_add_sync(FULL, pend);
+        const u32 hi = __reduce_max_sync(FULL, (u32)(best >> 32));
+        const u32 lo = __reduce_max_sync(FULL, (u32)(best >> 32) == hi ? (u32)best : 0u);
+        if (lane == 0) {
+          sm.pcnt[l] = pend;
+          sm.sent[l] = ((unsigned long long)hi << 32) | lo;
         }
       }
       __syncwarp();
-      if (__any_sync(FULL, got)) {
-        ns = 32;
-      } else {
-        __nanosleep(ns);
-        ns = ns < 256 ? ns * 2 : ns;
-      }
     }
     __syncwarp();
+    if (a.trace && lane == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      a.trace[4 * chunk + 0] = t_claim;
+      a.trace[4 * chunk + 1] = t_a;
+      a.trace[4 * chunk + 2] = gtimer();
+      a.trace[4 * chunk + 3] = smid;
+    }
   }
 }
 
@@ -337,9 +424,22 @@ void launch_gs(const GsLaunch& L, cudaStream_t s) {
   a.nwl = L.nwl_dev;
   a.prio = L.prio;
   a.ticket = L.ticket;
+  a.trace = nullptr;
+  a.vtrace = nullptr;
   CUDA_CHECK(cudaMemsetAsync(L.ticket, 0, sizeof(unsigned long long), s));
   const i64 nchunks = (L.nwl_max + 31) / 32;
-  const int blocks_per_sm = 4;
+  static const char* trace_path = std::getenv("CHROMA_GS_TRACE");
+  static const int bps_env = std::getenv("CHROMA_GS_BPS") ? std::atoi(std::getenv("CHROMA_GS_BPS")) : 0;
+  DBuf<unsigned long long> tr, vtr;
+  if (trace_path) {
+    tr.alloc(4 * nchunks, s);
+    tr.zero(s);
+    a.trace = tr.p;
+    vtr.alloc(32 * nchunks, s);
+    vtr.zero(s);
+    a.vtrace = vtr.p;
+  }
+  const int blocks_per_sm = bps_env > 0 ? bps_env : 8;
   int grid = (int)std::min<i64>((nchunks + WARPS - 1) / WARPS, (i64)num_sms() * blocks_per_sm);
   if (grid < 1) grid = 1;
   if (L.dist == 1)
@@ -350,6 +450,22 @@ void launch_gs(const GsLaunch& L, cudaStream_t s) {
     gs_kernel<2, false><<<grid, WARPS * 32, 0, s>>>(a);
   count_launch();
   CUDA_CHECK(cudaGetLastError());
+  if (trace_path) {
+    std::vector<unsigned long long> h((size_t)(4 * nchunks));
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), tr.p, sizeof(unsigned long long) * 4 * nchunks, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (FILE* f = std::fopen(trace_path, "wb")) {
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      std::fclose(f);
+    }
+    std::vector<unsigned long long> hv((size_t)(32 * nchunks));
+    CUDA_CHECK(cudaMemcpyAsync(hv.data(), vtr.p, sizeof(unsigned long long) * 32 * nchunks, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (FILE* f = std::fopen((std::string(trace_path) + ".v").c_str(), "wb")) {
+      std::fwrite(hv.data(), sizeof(unsigned long long), hv.size(), f);
+      std::fclose(f);
+    }
+  }
 }
 
 }  // namespace chroma

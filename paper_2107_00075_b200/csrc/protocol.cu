@@ -30,14 +30,27 @@ __global__ void k_flag_worklist(const i32* colors, const uint8_t* owned_flag, i6
     flag[i] = (colors[i] == 0 && (!owned_only || owned_flag[i])) ? 1 : 0;
 }
 
-// recolored_per_rank: owned entries of the worklist per local rank
+// recolored_per_rank: owned entries of the worklist per local rank (block-local
+// histogram in shared memory, one global atomic per block and rank)
 __global__ void k_count_recolored(const i32* wl, const i64* nwl, const uint8_t* owned_flag,
-                                  const i32* rank_of, i32 rank_lo, unsigned long long* stats) {
+                                  const i32* rank_of, i32 rank_lo, i32 nlocal, unsigned long long* stats) {
+  __shared__ unsigned long long h[256];
+  const bool local_hist = nlocal <= 256;
+  if (local_hist)
+    for (int i = threadIdx.x; i < nlocal; i += blockDim.x) h[i] = 0;
+  __syncthreads();
   const i64 n = *nwl;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 v = wl[i];
-    if (owned_flag[v]) atomicAdd(&stats[3 + rank_lo + rank_of[v]], 1ull);
+    if (owned_flag[v]) {
+      if (local_hist) atomicAdd(&h[rank_of[v]], 1ull);
+      else atomicAdd(&stats[3 + rank_lo + rank_of[v]], 1ull);
+    }
   }
+  __syncthreads();
+  if (local_hist)
+    for (int i = threadIdx.x; i < nlocal; i += blockDim.x)
+      if (h[i]) atomicAdd(&stats[3 + rank_lo + i], h[i]);
 }
 
 __global__ void k_set_u8_idx(uint8_t* flags, const i32* idx, const i64* n_dev, uint8_t v) {
@@ -269,7 +282,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     count_launch();
     select_flagged(w.cs.flags.p, w.NL, w.cs.wl.p, w.cs.nwl.p, s);
     k_count_recolored<<<G(w.NL), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
-                                              w.stats.p);
+                                              w.rank_hi - w.rank_lo, w.stats.p);
     count_launch();
     const bool gs_like = algo != CHROMA_ALGO_JACOBI;
     color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, w.NL, true, dist, partial,

@@ -203,11 +203,23 @@ __global__ void k_maxc(const i32* c, i64 n, int* mx) {
   m = __reduce_max_sync(FULL, m);
   if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
 }
-__global__ void k_hist(const i32* c, i64 n, unsigned long long* h) {
+__global__ void k_hist(const i32* c, i64 n, int maxc, unsigned long long* h) {
+  __shared__ unsigned long long sh[1024];
+  const bool loc = maxc < 1024;
+  if (loc)
+    for (int i = threadIdx.x; i <= maxc; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 x = c[i];
-    if (x > 0) atomicAdd(&h[x], 1ull);
+    if (x > 0) {
+      if (loc) atomicAdd(&sh[x], 1ull);
+      else atomicAdd(&h[x], 1ull);
+    }
   }
+  __syncthreads();
+  if (loc)
+    for (int i = threadIdx.x; i <= maxc; i += blockDim.x)
+      if (sh[i]) atomicAdd(&h[i], sh[i]);
 }
 }  // namespace
 
@@ -228,7 +240,7 @@ void run_color_stats(const i32* colors, i64 n, i64* num_colors, i64* max_color, 
   h.alloc(hm + 1, s);
   h.zero(s);
   if (n > 0 && hm > 0) {
-    k_hist<<<g, 256, 0, s>>>(colors, n, h.p);
+    k_hist<<<g, 256, 0, s>>>(colors, n, hm, h.p);
     count_launch();
   }
   std::vector<unsigned long long> hh(hm + 1);

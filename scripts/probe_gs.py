@@ -1,0 +1,38 @@
+"""Dev probe: GS colouring kernel time on BASELINE-like shapes (+ oracle check)."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import ctypes as C
+import numpy as np
+import oracle
+from paper_2107_00075_b200 import graph as G, partition as PT, runtime as RT, protocol as R, _lib
+
+def run(name, g, mode, check=True, reps=3, P=1, algorithm=None):
+    t0 = time.perf_counter()
+    w = RT.build_local_graphs(g, PT.partition_block(g, P), R.ghost_layers_for(R.Mode(mode)))
+    tb = time.perf_counter() - t0
+    cfg = R.AlgorithmConfig(mode=R.Mode(mode), deterministic=algorithm is None, algorithm=algorithm)
+    tb5 = (C.c_double * 5)()
+    best = None
+    for _ in range(reps):
+        colors, reps_ = R.run_distributed(w, cfg)
+        _lib.lib().chroma_world_last_timing(w.handle.h, tb5)
+        t = list(tb5)
+        best = t if best is None or t[0] < best[0] else best
+    ok = ""
+    if check:
+        ow = oracle.World(g.row_offsets, g.col_indices, PT.partition_block(g, P).owner, P, R.ghost_layers_for(R.Mode(mode)))
+        ref, _ = ow.run(mode, False, True)
+        ok = "EXACT" if np.array_equal(ref, colors) else "MISMATCH"
+    print(f"{name:28s} {mode:6s} P={P} n={g.num_vertices:9d} m={len(g.col_indices)//2:10d} build={tb*1e3:8.1f}ms "
+          f"total={best[0]*1e3:8.3f}ms kernel={best[1]*1e3:8.3f}ms detect={best[4]*1e3:7.3f}ms rounds={len(reps_)} "
+          f"colors={colors.max()} {ok}", flush=True)
+
+which = sys.argv[1:] or ["c1", "c2", "rmat18", "d2_100", "pd2_16", "c2p4"]
+if "c1" in which: run("grid 1000^2", G.gen_hex_mesh(1000, 1000, 1), "d1")
+if "c2" in which: run("27pt 128^3", G.gen_stencil27(128, device="cuda"), "d1-2gl")
+if "c2p4" in which: run("27pt 128^3", G.gen_stencil27(128, device="cuda"), "d1-2gl", P=4)
+if "rmat18" in which: run("rmat s18", G.gen_rmat(18, 16, 1, device="cuda"), "d1", check=True)
+if "rmat20" in which: run("rmat s20", G.gen_rmat(20, 16, 1, device="cuda"), "d1", check=True)
+if "d2_100" in which: run("7pt 100^3", G.gen_hex_mesh(100, 100, 100), "d2")
+if "pd2_16" in which: run("pd2 2^16 rows", G.gen_random_bipartite(1 << 16, 32, 3, device="cuda").graph, "pd2")
+if "pd2_18" in which: run("pd2 2^18 rows", G.gen_random_bipartite(1 << 18, 32, 3, device="cuda").graph, "pd2", check=False)
