@@ -190,6 +190,7 @@ int chroma_serial_greedy(chroma_csr* h, const int64_t* order, int32_t* colors_ou
     L.prio = order ? prio.p : nullptr;
     L.ticket = S.ticket.p;
     L.dist = 1;
+    L.nv = n;
     if (n > 0) launch_gs(L, s);
     CUDA_CHECK(cudaMemcpyAsync(colors_out, S.val.p, sizeof(i32) * n,
                                dev(flags) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));

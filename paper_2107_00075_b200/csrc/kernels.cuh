@@ -21,6 +21,7 @@ struct GsLaunch {
   unsigned long long* ticket = nullptr;
   int dist = 1;
   bool partial = false;
+  i64 nv = 0;                  // number of vertices (ids are < nv)
 };
 void launch_gs(const GsLaunch& L, cudaStream_t s);
 

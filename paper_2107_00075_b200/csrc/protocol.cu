@@ -125,6 +125,7 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     L.ticket = S.ticket.p;
     L.dist = dist;
     L.partial = partial;
+    L.nv = nv;
     if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
     launch_gs(L, s);
     if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
