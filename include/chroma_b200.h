@@ -129,8 +129,13 @@ int chroma_world_rank_arrays(chroma_world* w, int32_t rank, int64_t* row_offsets
  * owned vertices to peer p listed in send_lids (peer-major, in the order the peer
  * expects), recv_counts[p] ghost slots from peer p listed in recv_lids.  This is the
  * precomputed form of chroma/runtime.py:249-256 send_targets. */
+typedef struct chroma_comm chroma_comm;   /* an NCCL communicator (one per process) */
 int chroma_nccl_unique_id(void* id_out_128);
-int chroma_world_connect(chroma_world* w, const void* nccl_id_128, int32_t nranks, int32_t rank,
+int chroma_comm_create(const void* nccl_id_128, int32_t nranks, int32_t rank, int device,
+                       chroma_comm** out);
+int chroma_comm_destroy(chroma_comm* c);
+/* The world borrows `comm` (which must outlive it). */
+int chroma_world_connect(chroma_world* w, chroma_comm* comm, int32_t nranks, int32_t rank,
                          const int64_t* send_counts, const int64_t* send_lids,
                          const int64_t* recv_counts, const int64_t* recv_lids);
 

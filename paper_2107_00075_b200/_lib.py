@@ -58,6 +58,8 @@ def lib():
         "chroma_world_rank_info": (I, [P, i32, P]),
         "chroma_world_rank_arrays": (I, [P, i32, P, P, P, P, P, P]),
         "chroma_nccl_unique_id": (I, [P]),
+        "chroma_comm_create": (I, [P, i32, i32, I, C.POINTER(P)]),
+        "chroma_comm_destroy": (I, [P]),
         "chroma_world_connect": (I, [P, P, i32, i32, P, P, P, P]),
         "chroma_world_global_degrees": (I, [P, i32, P]),
         "chroma_world_reset_exchange": (I, [P]),
@@ -82,6 +84,7 @@ EXPORTS = ("chroma_last_error", "chroma_version", "chroma_device_count", "chroma
            "chroma_serial_greedy", "chroma_color", "chroma_detect", "chroma_verify",
            "chroma_color_stats", "chroma_world_create", "chroma_world_destroy",
            "chroma_world_rank_info", "chroma_world_rank_arrays", "chroma_nccl_unique_id",
+           "chroma_comm_create", "chroma_comm_destroy",
            "chroma_world_connect", "chroma_world_global_degrees", "chroma_world_reset_exchange",
            "chroma_world_exchange", "chroma_world_color", "chroma_world_detect",
            "chroma_run_distributed", "chroma_world_colors_device", "chroma_world_last_timing",

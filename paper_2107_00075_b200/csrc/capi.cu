@@ -11,7 +11,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
                     chroma_round_report* reports, i64* recolored, i64 cap, i64* n_reports,
                     bool out_on_device);
 #ifdef CHROMA_WITH_NCCL
-void world_connect(World& w, const void* id_bytes, i32 nranks, i32 rank, const i64* send_counts,
+void world_connect(World& w, void* comm, i32 nranks, i32 rank, const i64* send_counts,
                    const i64* send_lids, const i64* recv_counts, const i64* recv_lids);
 #endif
 
@@ -27,6 +27,12 @@ struct chroma_csr {
 };
 struct chroma_world {
   World* w = nullptr;
+};
+struct chroma_comm {
+#ifdef CHROMA_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  int nranks = 0, rank = 0;
 };
 
 template <typename F>
@@ -384,13 +390,45 @@ int chroma_nccl_unique_id(void* id_out) {
   });
 }
 
-int chroma_world_connect(chroma_world* h, const void* id, int32_t nranks, int32_t rank, const int64_t* sc,
+int chroma_comm_create(const void* id_bytes, int32_t nranks, int32_t rank, int device, chroma_comm** out) {
+  return guarded([&] {
+#ifdef CHROMA_WITH_NCCL
+    CUDA_CHECK(cudaSetDevice(device));
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, sizeof(id));
+    auto* c = new chroma_comm();
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      delete c;
+      throw Error(CHROMA_ECUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    c->nranks = nranks;
+    c->rank = rank;
+    *out = c;
+#else
+    (void)id_bytes; (void)nranks; (void)rank; (void)device; (void)out;
+    throw Error(CHROMA_ECUDA, "built without NCCL");
+#endif
+  });
+}
+
+int chroma_comm_destroy(chroma_comm* c) {
+  return guarded([&] {
+#ifdef CHROMA_WITH_NCCL
+    if (c) ncclCommDestroy(c->comm);
+#endif
+    delete c;
+  });
+}
+
+int chroma_world_connect(chroma_world* h, chroma_comm* c, int32_t nranks, int32_t rank, const int64_t* sc,
                          const int64_t* sl, const int64_t* rc, const int64_t* rl) {
   return guarded([&] {
 #ifdef CHROMA_WITH_NCCL
-    world_connect(*h->w, id, nranks, rank, sc, sl, rc, rl);
+    CHROMA_REQUIRE(c && c->nranks == nranks && c->rank == rank, CHROMA_EVALUE, "communicator does not match");
+    world_connect(*h->w, (void*)c->comm, nranks, rank, sc, sl, rc, rl);
 #else
-    (void)h; (void)id; (void)nranks; (void)rank; (void)sc; (void)sl; (void)rc; (void)rl;
+    (void)h; (void)c; (void)nranks; (void)rank; (void)sc; (void)sl; (void)rc; (void)rl;
     throw Error(CHROMA_ECUDA, "built without NCCL");
 #endif
   });

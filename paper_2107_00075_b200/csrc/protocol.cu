@@ -363,7 +363,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
 // Install the static halo routing computed by the host (dist.build_routing: ghost
 // slots grouped by owner; owned lids each peer asked for) and create this rank's
 // NCCL communicator.  All lists are in local ids of this process's single rank.
-void world_connect(World& w, const void* id_bytes, i32 nranks, i32 rank, const i64* send_counts,
+void world_connect(World& w, void* comm, i32 nranks, i32 rank, const i64* send_counts,
                    const i64* send_lids, const i64* recv_counts, const i64* recv_lids) {
   CHROMA_REQUIRE(nranks == w.P, CHROMA_EVALUE, "communicator size differs from num_ranks");
   CHROMA_REQUIRE(w.rank_hi - w.rank_lo == 1 && w.rank_lo == rank, CHROMA_EVALUE,
@@ -415,9 +415,7 @@ void world_connect(World& w, const void* id_bytes, i32 nranks, i32 rank, const i
   w.recvbuf.alloc(std::max<i64>(w.nrecv, 1), s);
   CUDA_CHECK(cudaMemsetAsync(w.changed.p, 0, w.NL + 1, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
-  ncclUniqueId id;
-  std::memcpy(&id, id_bytes, sizeof(id));
-  NCCL_CHECK(ncclCommInitRank(&w.comm, nranks, id, rank));
+  w.comm = (ncclComm_t)comm;
   w.my_rank = rank;
   w.connected = true;
   world_reset_exchange(w);

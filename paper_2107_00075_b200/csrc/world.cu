@@ -502,10 +502,7 @@ void world_destroy(World* w) {
   cudaSetDevice(w->device);
   cudaStream_t s = w->stream;
   if (s) cudaStreamSynchronize(s);
-#ifdef CHROMA_WITH_NCCL
-  if (w->comm) ncclCommDestroy(w->comm);
-#endif
-  delete w;
+  delete w;  // the NCCL communicator is borrowed (chroma_comm), not owned
   if (s) cudaStreamDestroy(s);
 }
 

@@ -80,6 +80,40 @@ def torch_alltoallv(group=None, device=None):
     return run
 
 
+class Communicator:
+    """This process's NCCL communicator inside libchroma_b200 (chroma_comm)."""
+
+    def __init__(self, id_bytes: bytes, nranks: int, rank: int, device: int):
+        buf = (C.c_char * 128).from_buffer_copy(id_bytes)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().chroma_comm_create(buf, nranks, rank, device, C.byref(h)), "chroma_comm_create")
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and _lib._lib is not None:
+            _lib._lib.chroma_comm_destroy(h)
+            self.h = None
+
+
+_COMMS: dict = {}
+
+
+def communicator(group, nranks: int, rank: int, device: int) -> Communicator:
+    """One communicator per (process group, device), created once: worlds borrow it."""
+    import torch.distributed as dist
+    key = (id(group), nranks, rank, device)
+    c = _COMMS.get(key)
+    if c is None:
+        idbuf = (C.c_char * 128)()
+        if rank == 0:
+            _lib.check(_lib.lib().chroma_nccl_unique_id(idbuf))
+        obj = [bytes(idbuf) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        c = _COMMS[key] = Communicator(obj[0], nranks, rank, device)
+    return c
+
+
 class DistWorld:
     """This process's rank of a num_ranks-way partition, on its own GPU."""
 
@@ -109,14 +143,9 @@ class DistWorld:
         lg = self.local_graph
         routing = build_routing(lg.gids, lg.owned_count, lg.ghost_owner, self.num_ranks, self.rank,
                                 torch_alltoallv(group, device=f"cuda:{self.device}"))
-        idbuf = (C.c_char * 128)()
-        if self.rank == 0:
-            _lib.check(_lib.lib().chroma_nccl_unique_id(idbuf))
-        obj = [bytes(idbuf) if self.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        idbuf = (C.c_char * 128).from_buffer_copy(obj[0])
+        self.comm = communicator(group, self.num_ranks, self.rank, self.device)
         sc, sl, rc, rl = (_lib.i64(x) for x in routing)
-        _lib.check(_lib.lib().chroma_world_connect(self.handle.h, idbuf, self.num_ranks, self.rank,
+        _lib.check(_lib.lib().chroma_world_connect(self.handle.h, self.comm.h, self.num_ranks, self.rank,
                                                    _lib.ptr(sc), _lib.ptr(sl), _lib.ptr(rc), _lib.ptr(rl)),
                    "chroma_world_connect")
         self.halo_send = int(sc.sum())
