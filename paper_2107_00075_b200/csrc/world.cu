@@ -30,6 +30,36 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// partition_block (chroma/partition.py:49-58): owner[v] = r for v in [rn/P, (r+1)n/P)
+__global__ void k_block_owner(i32* owner, i64 n, i32 P) {
+  for (i64 v = blockIdx.x * (i64)blockDim.x + threadIdx.x; v < n; v += (i64)gridDim.x * blockDim.x) {
+    i64 r = (v * P) / n;
+    while (r + 1 < P && ((r + 1) * n) / P <= v) r++;
+    while (r > 0 && (r * n) / P > v) r--;
+    owner[v] = (i32)r;
+  }
+}
+
+// chk[0] += out-of-range owners, chk[1] = max degree, chk[2 + r] += |owned(r)|
+__global__ void k_owner_check(const i32* owner, i64 n, i32 P, const i64* off, unsigned long long* chk) {
+  unsigned long long bad = 0, dmax = 0;
+  for (i64 v = blockIdx.x * (i64)blockDim.x + threadIdx.x; v < n; v += (i64)gridDim.x * blockDim.x) {
+    const i32 o = owner[v];
+    if (o < 0 || o >= P) bad++;
+    else if (P <= 4096) atomicAdd(&chk[2 + o], 1ull);
+    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
+    dmax = d > dmax ? d : dmax;
+  }
+  if (bad) atomicAdd(&chk[0], bad);
+  atomicMax(&chk[1], dmax);
+}
+
+// owned_lid[list[i]] = i (position of each owned gid inside its owner)
+__global__ void k_scatter_pos(const i32* list, i64 k, i32* pos) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < k; i += (i64)gridDim.x * blockDim.x)
+    pos[list[i]] = (i32)i;
+}
+
 __global__ void k_i64_to_i32(const i64* in, i32* out, i64 n) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
     out[i] = (i32)in[i];
@@ -249,25 +279,6 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
   CHROMA_REQUIRE(n >= 0 && n < ((i64)1 << 31) - 1, CHROMA_EVALUE, "graph too large for int32 local ids");
   CHROMA_REQUIRE(0 <= lo && lo < hi && hi <= P, CHROMA_EVALUE, "bad local rank range");
   const i64 nnz = h_off[n];
-  // partition validation (chroma/partition.py:36-43, chroma/runtime.py:159-161)
-  std::vector<i32> owner_v((size_t)n);
-  std::vector<i64> counts((size_t)P, 0);
-  for (i64 v = 0; v < n; v++) {
-    const i32 o = h_owner ? h_owner[v] : (i32)0;
-    CHROMA_REQUIRE(o >= 0 && o < P, CHROMA_EVALUE, "owner out of range");
-    owner_v[(size_t)v] = o;
-    counts[(size_t)o]++;
-  }
-  if (P <= n)
-    for (i32 r = 0; r < P; r++)
-      CHROMA_REQUIRE(counts[(size_t)r] > 0, CHROMA_EVALUE, "empty rank with num_ranks <= num_vertices");
-  std::vector<i32> owned_lid_h((size_t)n);
-  {
-    std::vector<i64> c((size_t)P, 0);
-    for (i64 v = 0; v < n; v++) owned_lid_h[(size_t)v] = (i32)c[(size_t)owner_v[(size_t)v]]++;
-  }
-  i64 dmax = 0;
-  for (i64 v = 0; v < n; v++) dmax = std::max(dmax, h_off[v + 1] - h_off[v]);
 
   CUDA_CHECK(cudaSetDevice(device));
   World* w = new World();
@@ -276,10 +287,35 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
     CUDA_CHECK(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
     cudaStream_t s = w->stream;
     w->P = P; w->rank_lo = lo; w->rank_hi = hi; w->gl = gl;
-    w->n_global = n; w->m_global = nnz / 2; w->delta_max = dmax;
+    w->n_global = n; w->m_global = nnz / 2;
 
     DBuf<i64> goff;
     goff.upload(h_off, n + 1, s);
+    // owner: uploaded (any PartitionMap) or computed (partition_block when h_owner is NULL);
+    // validated on the device (chroma/partition.py:36-43, chroma/runtime.py:159-161)
+    DBuf<i32> owner;
+    if (h_owner) {
+      owner.upload(h_owner, std::max<i64>(n, 1), s);
+    } else {
+      owner.alloc(std::max<i64>(n, 1), s);
+      k_block_owner<<<G(n), 256, 0, s>>>(owner.p, n, P);
+      count_launch();
+    }
+    {
+      DBuf<unsigned long long> chk;
+      chk.alloc(P + 2, s);
+      chk.zero(s);
+      k_owner_check<<<G(n), 256, 0, s>>>(owner.p, n, P, goff.p, chk.p);
+      count_launch();
+      std::vector<unsigned long long> hc((size_t)P + 2);
+      CUDA_CHECK(cudaMemcpyAsync(hc.data(), chk.p, sizeof(unsigned long long) * (P + 2), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      CHROMA_REQUIRE(hc[0] == 0, CHROMA_EVALUE, "owner out of range");
+      if (P <= n && P <= 4096)
+        for (i32 r = 0; r < P; r++)
+          CHROMA_REQUIRE(hc[(size_t)r + 2] > 0, CHROMA_EVALUE, "empty rank with num_ranks <= num_vertices");
+      w->delta_max = (i64)hc[1];
+    }
     DBuf<i32> gcol;
     gcol.alloc(std::max<i64>(nnz, 1), s);
     {
@@ -293,9 +329,8 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
         count_launch();
       }
     }
-    DBuf<i32> owner, owned_lid, lid_of;
-    owner.upload(owner_v.data(), n, s);
-    owned_lid.upload(owned_lid_h.data(), n, s);
+    DBuf<i32> owned_lid, lid_of;
+    owned_lid.alloc(std::max<i64>(n, 1), s);  // gid -> lid inside its owner (filled per rank below)
     lid_of.alloc(std::max<i64>(n, 1), s);
     launch_fill_i32(lid_of.p, n, -1, s);
     DBuf<uint8_t> cls, flag;
@@ -324,7 +359,8 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       select_flagged(flag.p, n, T.lgids.p, cnt.p, s);
       const i64 oc = count_of(cnt.p);
       k_assign<<<G(oc), 256, 0, s>>>(T.lgids.p, oc, 0, 1, lid_of.p, cls.p);
-      count_launch();
+      k_scatter_pos<<<G(oc), 256, 0, s>>>(T.lgids.p, oc, owned_lid.p);
+      count_launch(2);
       // layer 1 = neighbours of owned not owned (ascending gid)
       k_mark_nbrs<<<GW(oc), 256, 0, s>>>(T.lgids.p, oc, goff.p, gcol.p, cls.p, 2);
       count_launch();

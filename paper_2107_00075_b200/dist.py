@@ -18,8 +18,8 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .graph import stats as graph_stats
-from .runtime import LocalGraph, ProtocolError, WorldHandle
+
+from .runtime import LocalGraph, ProtocolError, WorldHandle, device_stats
 
 __all__ = ["build_routing", "DistWorld", "torch_alltoallv"]
 
@@ -122,7 +122,8 @@ class DistWorld:
         import torch.distributed as dist
         if ghost_layers not in (1, 2):
             raise ValueError("ghost_layers must be 1 or 2")
-        pm.validate()
+        if pm.num_ranks < 1:
+            raise ValueError("num_ranks must be >= 1")
         if len(pm.owner) != g.num_vertices:
             raise ValueError("partition size does not match graph")
         self.rank = dist.get_rank(group) if rank is None else rank
@@ -134,8 +135,9 @@ class DistWorld:
         self.ghost_layers = ghost_layers
         self.partition = pm
         self.num_global_vertices = g.num_vertices
-        self.source_stats = graph_stats(g)
+        # owner validation happens in the device builder (chroma_world_create)
         self.handle = WorldHandle(g, pm, ghost_layers, self.rank, self.rank + 1, self.device)
+        self.source_stats = device_stats(self.handle)
         self.local_graph = LocalGraph(self.handle, self.rank, ghost_layers)
         self.local_graphs = [self.local_graph]
         self.total_bytes = 0

@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .graph import GraphStats, stats as graph_stats
+from .graph import GraphStats
 from .partition import PartitionMap
 
 __all__ = ["LocalGraph", "RankWorld", "RoundReport", "ProtocolError", "build_local_graphs",
@@ -39,11 +39,13 @@ class WorldHandle:
     def __init__(self, g, pm, ghost_layers: int, rank_lo: int, rank_hi: int, device: int | None = None):
         off = _lib.i64(g.row_offsets)
         col = _lib.i64(g.col_indices)
-        owner = _lib.i32(pm.owner)
+        # partition_block maps are regenerated on the device (no owner array upload)
+        owner = None if getattr(pm, "_block", False) else _lib.i32(pm.owner)
         self.device = _lib.default_device() if device is None else device
         h = C.c_void_p()
         _lib.check(_lib.lib().chroma_world_create(int(g.num_vertices), _lib.ptr(off), _lib.ptr(col),
-                                                  int(pm.num_ranks), _lib.ptr(owner), int(ghost_layers),
+                                                  int(pm.num_ranks), _lib.ptr(owner) if owner is not None
+                                                  else None, int(ghost_layers),
                                                   int(rank_lo), int(rank_hi), self.device, C.byref(h)),
                    "build_local_graphs")
         self.h = h
@@ -189,17 +191,26 @@ class RankWorld:
             _lib.check(_lib.lib().chroma_world_reset_exchange(self.handle.h))
 
 
+def device_stats(wh: WorldHandle) -> GraphStats:
+    """GraphStats of the source graph (chroma/graph.py:380-385) from the device build."""
+    i = wh.info(wh.rank_lo)
+    n, m = i["n_global"], i["m_global"]
+    return GraphStats(n, m, (2.0 * m / n) if n else 0.0, i["delta_max"] if n else 0)
+
+
 def build_local_graphs(g, pm: PartitionMap, ghost_layers: int = 1) -> RankWorld:
     """Split g across pm's ranks with one or two ghost layers, on the GPU."""
     if ghost_layers not in (1, 2):
         raise ValueError("ghost_layers must be 1 or 2")
-    pm.validate()
+    if pm.num_ranks < 1:
+        raise ValueError("num_ranks must be >= 1")
     if len(pm.owner) != g.num_vertices:
         raise ValueError("partition size does not match graph")
+    # owner range / empty-rank validation (PartitionMap.validate) runs on the device
     wh = WorldHandle(g, pm, ghost_layers, 0, pm.num_ranks)
     lgs = [LocalGraph(wh, r, ghost_layers) for r in range(pm.num_ranks)]
     world = RankWorld(num_ranks=pm.num_ranks, ghost_layers=ghost_layers, local_graphs=lgs,
-                      partition=pm, num_global_vertices=g.num_vertices, source_stats=graph_stats(g),
+                      partition=pm, num_global_vertices=g.num_vertices, source_stats=device_stats(wh),
                       handle=wh)
     world.reset_exchange_state()
     return world
