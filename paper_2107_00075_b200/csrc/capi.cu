@@ -108,6 +108,7 @@ int chroma_csr_create(int64_t n, const int64_t* off, const int64_t* col, int dev
   return guarded([&] {
     CHROMA_REQUIRE(n >= 0 && n < INT32_MAX, CHROMA_EVALUE, "graph too large for int32 ids");
     CUDA_CHECK(cudaSetDevice(device));
+    retain_pool_memory(device);
     auto* h = new chroma_csr();
     try {
       h->g.device = device;

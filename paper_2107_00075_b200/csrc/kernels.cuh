@@ -5,6 +5,7 @@
 namespace chroma {
 
 void count_launch(int k = 1);
+void retain_pool_memory(int device);
 i64 launch_count();
 
 // ---------------------------------------------------------------- colouring

@@ -11,6 +11,20 @@ static std::atomic<long long> g_launches{0};
 void count_launch(int k) { g_launches += k; }
 i64 launch_count() { return (i64)g_launches.load(); }
 
+// Keep freed stream-ordered allocations in the device pool instead of returning
+// them to the driver: worlds are rebuilt per call in the e2e path and the default
+// release threshold (0) made every rebuild pay the page-mapping cost again.
+void retain_pool_memory(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+  done[device] = true;
+}
+
 int num_sms() {
   static int sms = 0;
   if (!sms) {

@@ -11,6 +11,9 @@
 // partition of each row by class (owned < L1 < L2) is the lid-sorted row.  The
 // class lists themselves come out sorted from an ordered compaction over gids.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
@@ -258,6 +261,23 @@ __global__ void k_gather_i32(const i32* src, const i32* idx, const i64* n_dev, i
     out[i] = src[idx[i]];
 }
 
+// CHROMA_BUILD_TIMING=1 prints the device builder's phase times (synchronising)
+struct PhaseTimer {
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(cudaStream_t st) : s(st), on(std::getenv("CHROMA_BUILD_TIMING") != nullptr) {
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[build] %-18s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 int G(i64 n) { return grid_for(std::max<i64>(n, 1), 256, num_sms() * 16); }
 int GW(i64 n) { return grid_for(std::max<i64>(n, 1) * 32, 256, num_sms() * 16); }
 
@@ -281,6 +301,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
   const i64 nnz = h_off[n];
 
   CUDA_CHECK(cudaSetDevice(device));
+  retain_pool_memory(device);
   World* w = new World();
   try {
     w->device = device;
@@ -289,6 +310,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
     w->P = P; w->rank_lo = lo; w->rank_hi = hi; w->gl = gl;
     w->n_global = n; w->m_global = nnz / 2;
 
+    PhaseTimer ptm(s);
     DBuf<i64> goff;
     goff.upload(h_off, n + 1, s);
     // owner: uploaded (any PartitionMap) or computed (partition_block when h_owner is NULL);
@@ -316,6 +338,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
           CHROMA_REQUIRE(hc[(size_t)r + 2] > 0, CHROMA_EVALUE, "empty rank with num_ranks <= num_vertices");
       w->delta_max = (i64)hc[1];
     }
+    ptm.mark("offsets+owner");
     DBuf<i32> gcol;
     gcol.alloc(std::max<i64>(nnz, 1), s);
     {
@@ -329,6 +352,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
         count_launch();
       }
     }
+    ptm.mark("col h2d+convert");
     DBuf<i32> owned_lid, lid_of;
     owned_lid.alloc(std::max<i64>(n, 1), s);  // gid -> lid inside its owner (filled per rank below)
     lid_of.alloc(std::max<i64>(n, 1), s);
@@ -349,6 +373,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       CUDA_CHECK(cudaStreamSynchronize(s));
       return h;
     };
+    ptm.mark("scratch");
     for (i32 r = lo; r < hi; r++) {
       RankTmp& T = tmps[(size_t)(r - lo)];
       T.m.rank = r;
@@ -429,6 +454,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       count_launch();
     }
 
+    ptm.mark("rank builds");
     // ---- concatenate (block-diagonal local graphs)
     i64 NL = 0, NNZ = 0, NG = 0, NB1 = 0, NB2 = 0;
     for (auto& T : tmps) {
@@ -477,6 +503,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
     CUDA_CHECK(cudaStreamSynchronize(s));
     tmps.clear();
 
+    ptm.mark("concatenate");
     // ---- local routing (virtual ranks: every route has both ends in this process)
     if (w->all_local() && NG > 0) {
       std::vector<i64> lid_off_h((size_t)P);
@@ -521,6 +548,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       w->pair_cnt.alloc((i64)P * P, s);
       w->pair_cnt.zero(s);
     }
+    ptm.mark("routing");
     w->stats.alloc(3 + P, s);
     w->changed.alloc(NL + 1, s);
     world_reset_exchange(*w);

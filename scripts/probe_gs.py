@@ -36,3 +36,10 @@ if "rmat20" in which: run("rmat s20", G.gen_rmat(20, 16, 1, device="cuda"), "d1"
 if "d2_100" in which: run("7pt 100^3", G.gen_hex_mesh(100, 100, 100), "d2")
 if "pd2_16" in which: run("pd2 2^16 rows", G.gen_random_bipartite(1 << 16, 32, 3, device="cuda").graph, "pd2")
 if "pd2_18" in which: run("pd2 2^18 rows", G.gen_random_bipartite(1 << 18, 32, 3, device="cuda").graph, "pd2", check=False)
+if "jac" in which:
+    run("rmat s18 jacobi", G.gen_rmat(18, 16, 1, device="cuda"), "d1", check=False, algorithm="jacobi")
+    run("rmat s20 jacobi", G.gen_rmat(20, 16, 1, device="cuda"), "d1", check=False, algorithm="jacobi")
+    run("rmat s18 free", G.gen_rmat(18, 16, 1, device="cuda"), "d1", check=False, algorithm="free")
+    run("27pt 32^3 jacobi", G.gen_stencil27(32, device="cuda"), "d1-2gl", check=False, algorithm="jacobi")
+    run("rmat s18 jacobi P8", G.gen_rmat(18, 16, 1, device="cuda"), "d1", check=False, algorithm="jacobi", P=8)
+    run("rmat s18 gs P8", G.gen_rmat(18, 16, 1, device="cuda"), "d1", check=False, P=8)
