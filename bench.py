@@ -33,6 +33,28 @@ METRIC = "coloring edges/s (D1-2GL, 27-pt stencil 128^3)"
 UNIT = "edges/s"
 
 
+_JSON_FD = None
+
+
+def quiet_stdout():
+    """Route everything (Python prints, NCCL/C-level writes) to stderr so stdout
+    carries exactly the one JSON line."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -167,11 +189,12 @@ def run_reference(args):
                              "sample": f"oracle/ C port of the reference path, full workload each step, "
                                        f"1 of {os.cpu_count()} cores"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
     args = parse()
+    quiet_stdout()
     if args.impl == "reference":
         run_reference(args)
         return
@@ -268,6 +291,13 @@ def main():
     kernel_s = TK / args.steps
     peak, peak_kind = peaks()
     achieved = B / kernel_s / 1e9
+    traffic = None
+    if N == 1 and args.L == 128 and args.algorithm == "gauss-seidel":
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                traffic = json.load(fh)["gs_kernel_c2_p1"]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -312,11 +342,11 @@ def main():
                            "violations": nviol, "parallelism": f"vertex-range x{N}",
                            "l2": f"inputs larger than L2 (int32 col {4 * len(g.col_indices) / 1e6:.0f} MB)"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None, "kernel": "gs_kernel (colouring)",
+                             "frac": achieved / peak, "traffic": traffic, "kernel": "gs_kernel (colouring)",
                              "algorithmic_bytes_per_launch": B, "kernel_ms": kernel_s * 1e3,
                              "peak_kind": peak_kind},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if N > 1:
         dist.destroy_process_group()
 

@@ -358,21 +358,24 @@ int chroma_world_rank_arrays(chroma_world* h, int32_t rank, int64_t* off, int64_
     const RankMeta& m = w.meta(rank);
     cudaStream_t s = w.stream;
     CUDA_CHECK(cudaSetDevice(w.device));
+    // every output pointer may be NULL (that array is not copied)
     const i64 nl = m.owned + m.ghost;
-    std::vector<i64> o((size_t)nl + 1);
-    std::vector<i32> c((size_t)m.nnz), bb1((size_t)m.nb1), bb2((size_t)m.nb2);
-    CUDA_CHECK(cudaMemcpyAsync(o.data(), w.g.rowptr.p + m.lid_off, sizeof(i64) * (nl + 1), cudaMemcpyDeviceToHost, s));
-    if (m.nnz) CUDA_CHECK(cudaMemcpyAsync(c.data(), w.g.col.p + m.nnz_off, sizeof(i32) * m.nnz, cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaMemcpyAsync(gids, w.gids.p + m.lid_off, sizeof(i64) * nl, cudaMemcpyDeviceToHost, s));
-    if (m.ghost)
+    std::vector<i64> o(off ? (size_t)nl + 1 : 0);
+    std::vector<i32> c(col ? (size_t)m.nnz : 0), bb1(b1 ? (size_t)m.nb1 : 0), bb2(b2 ? (size_t)m.nb2 : 0);
+    if (off)
+      CUDA_CHECK(cudaMemcpyAsync(o.data(), w.g.rowptr.p + m.lid_off, sizeof(i64) * (nl + 1), cudaMemcpyDeviceToHost, s));
+    if (col && m.nnz)
+      CUDA_CHECK(cudaMemcpyAsync(c.data(), w.g.col.p + m.nnz_off, sizeof(i32) * m.nnz, cudaMemcpyDeviceToHost, s));
+    if (gids) CUDA_CHECK(cudaMemcpyAsync(gids, w.gids.p + m.lid_off, sizeof(i64) * nl, cudaMemcpyDeviceToHost, s));
+    if (ghost_owner && m.ghost)
       CUDA_CHECK(cudaMemcpyAsync(ghost_owner, w.ghost_owner.p + m.ghost_off, sizeof(i32) * m.ghost, cudaMemcpyDeviceToHost, s));
-    if (m.nb1) CUDA_CHECK(cudaMemcpyAsync(bb1.data(), w.b1.p + m.b1_off, sizeof(i32) * m.nb1, cudaMemcpyDeviceToHost, s));
-    if (m.nb2) CUDA_CHECK(cudaMemcpyAsync(bb2.data(), w.b2.p + m.b2_off, sizeof(i32) * m.nb2, cudaMemcpyDeviceToHost, s));
+    if (b1 && m.nb1) CUDA_CHECK(cudaMemcpyAsync(bb1.data(), w.b1.p + m.b1_off, sizeof(i32) * m.nb1, cudaMemcpyDeviceToHost, s));
+    if (b2 && m.nb2) CUDA_CHECK(cudaMemcpyAsync(bb2.data(), w.b2.p + m.b2_off, sizeof(i32) * m.nb2, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-    for (i64 i = 0; i <= nl; i++) off[i] = o[(size_t)i] - m.nnz_off;
-    for (i64 i = 0; i < m.nnz; i++) col[i] = (i64)c[(size_t)i] - m.lid_off;
-    for (i64 i = 0; i < m.nb1; i++) b1[i] = (i64)bb1[(size_t)i] - m.lid_off;
-    for (i64 i = 0; i < m.nb2; i++) b2[i] = (i64)bb2[(size_t)i] - m.lid_off;
+    if (off) for (i64 i = 0; i <= nl; i++) off[i] = o[(size_t)i] - m.nnz_off;
+    if (col) for (i64 i = 0; i < m.nnz; i++) col[i] = (i64)c[(size_t)i] - m.lid_off;
+    if (b1) for (i64 i = 0; i < m.nb1; i++) b1[i] = (i64)bb1[(size_t)i] - m.lid_off;
+    if (b2) for (i64 i = 0; i < m.nb2; i++) b2[i] = (i64)bb2[(size_t)i] - m.lid_off;
   });
 }
 

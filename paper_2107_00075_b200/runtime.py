@@ -89,20 +89,25 @@ class LocalGraph:
         self._gid_to_lid: dict | None = None
         self.global_degrees: np.ndarray | None = None
 
-    def _fetch(self) -> dict:
+    def _fetch(self, name: str) -> np.ndarray:
+        """One LocalGraph array, copied from the device on first use."""
         if self._arrays is None:
+            self._arrays = {}
+        if name not in self._arrays:
             nl = self.num_local
-            a = {"row_offsets": np.zeros(nl + 1, np.int64), "col_indices": np.zeros(self._nnz, np.int64),
-                 "gids": np.zeros(nl, np.int64), "ghost_owner": np.zeros(self.ghost_count, np.int32),
-                 "boundary_d1": np.zeros(self._nb1, np.int64), "boundary_d2": np.zeros(self._nb2, np.int64)}
-            _lib.check(_lib.lib().chroma_world_rank_arrays(
-                self._wh.h, self.rank, *(_lib.ptr(a[k]) for k in self._ARRAYS)))
-            self._arrays = a
-        return self._arrays
+            shapes = {"row_offsets": (nl + 1, np.int64), "col_indices": (self._nnz, np.int64),
+                      "gids": (nl, np.int64), "ghost_owner": (self.ghost_count, np.int32),
+                      "boundary_d1": (self._nb1, np.int64), "boundary_d2": (self._nb2, np.int64)}
+            size, dt = shapes[name]
+            arr = np.zeros(size, dt)
+            ptrs = [_lib.ptr(arr) if k == name else None for k in self._ARRAYS]
+            _lib.check(_lib.lib().chroma_world_rank_arrays(self._wh.h, self.rank, *ptrs))
+            self._arrays[name] = arr
+        return self._arrays[name]
 
     def __getattr__(self, name):
         if name in LocalGraph._ARRAYS:
-            return self._fetch()[name]
+            return self._fetch(name)
         raise AttributeError(name)
 
     @property
