@@ -414,6 +414,9 @@ gs_kernel(GsArgs a) {
 }  // namespace
 
 void launch_gs(const GsLaunch& L, cudaStream_t s) {
+  // distance 1 in id order: the pre-scan-free kernel (color_gs_d1.cu)
+  static const bool generic = std::getenv("CHROMA_GS_GENERIC") != nullptr;
+  if (!generic && launch_gs_d1(L, s)) return;
   GsArgs a;
   a.rowptr = L.rowptr;
   a.col = L.col;

@@ -25,6 +25,7 @@ struct GsLaunch {
   i64 nv = 0;                  // number of vertices (ids are < nv)
 };
 void launch_gs(const GsLaunch& L, cudaStream_t s);
+bool launch_gs_d1(const GsLaunch& L, cudaStream_t s);  // false if not applicable
 
 // Jacobi sweep pieces (chroma/localcolor.py:214-227, 292-303)
 void launch_jacobi_propose(const i64* rowptr, const i32* col, const i32* colors, const i32* pending,
