@@ -35,6 +35,31 @@ void launch_jacobi_losers(const i64* rowptr, const i32* col, i32* colors, const 
                           const i64* np_dev, i64 np_max, const i32* prop, const uint8_t* in_round,
                           uint8_t* lose, int dist, bool partial, cudaStream_t s);
 
+// Free-running speculative colouring (deterministic=False, algorithm="free").
+// Pending vertices are kept in light (warp per vertex) and heavy (CTA per vertex)
+// lists, double-buffered by parity p; cnt[2p] / cnt[2p+1] are their lengths.
+struct FreeLists {
+  i32* light[2];
+  i32* heavy[2];
+  i64* cnt;  // [4]
+};
+struct FreeWaveScratch {
+  DBuf<u32> F, A;
+  DBuf<int> ovf;
+  DBuf<unsigned> bar;
+  DBuf<u64> dbg;
+};
+// Exact wave colouring of the heavy list (sorted in place); vertices whose colour
+// would exceed the heavy mask are appended to light[*nlight].
+void launch_free_heavy(const i64* rowptr, const i32* col, i32* colors, i32* heavy, i64 n, i32* light,
+                       i64* nlight, int dist, bool partial, FreeWaveScratch& ws, cudaStream_t s);
+void launch_free_split(const i32* wl, const i64* n_dev, i64 n_max, const i64* rowptr, i64 heavy_deg, FreeLists& f,
+                       int p, cudaStream_t s);
+// colour lists[p] (rank_cap > 0: snapshot rank-offset first fit, skipping up to
+// rank_cap free colours), resolve, losers -> lists[p^1]
+void launch_free_iteration(const i64* rowptr, const i32* col, i32* colors, FreeLists& f, int p, i64 nlight_max,
+                           i64 nheavy_max, int rank_cap, int dist, bool partial, cudaStream_t s);
+
 // ---------------------------------------------------------------- utilities
 void launch_fill_i32(i32* p, i64 n, i32 v, cudaStream_t s);
 void launch_iota_i32(i32* p, i64 n, i32 base, cudaStream_t s);

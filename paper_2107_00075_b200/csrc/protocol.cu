@@ -13,6 +13,8 @@
 // than every owned vertex, so their sequential recolouring can only affect other
 // ghosts, which the restore/exchange overwrites.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
@@ -75,6 +77,11 @@ i64 read_i64(const i64* d, cudaStream_t s) {
 
 constexpr int MAX_SWEEPS = 10000;  // chroma/localcolor.py:34
 
+i64 env_i64(const char* name, i64 dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoll(v) : dflt;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ colouring driver
@@ -101,7 +108,58 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     nwl = S.nwl.p;
     nwl_max = k;
   }
-  if (algo == CHROMA_ALGO_GAUSS_SEIDEL || algo == CHROMA_ALGO_FREE) {
+  if (algo == CHROMA_ALGO_FREE) {
+    // color_free.cu: in-place first fit -> larger id keeps its colour -> the losers
+    // iterate with snapshot rank-offset first fit until none is left
+    i32* cur = colors;
+    if (!colors_nonneg) {
+      S.val.reserve(nv, s);
+      launch_clamp_nonneg(S.val.p, colors, nv, s);
+      cur = S.val.p;
+    }
+    launch_scatter_const(cur, wl, nwl, nwl_max, 0, s);
+    for (auto& b : S.fl) b.reserve(nwl_max, s);
+    S.fcnt.reserve(4, s);
+    FreeLists f{{S.fl[0].p, S.fl[1].p}, {S.fl[2].p, S.fl[3].p}, S.fcnt.p};
+    static const i64 heavy_deg = env_i64("CHROMA_FREE_HEAVY", 1024);
+    static const i64 rank_cap = env_i64("CHROMA_FREE_RANKCAP", 0);
+    static const bool trace = std::getenv("CHROMA_FREE_TRACE") != nullptr;
+    static const bool no_waves = std::getenv("CHROMA_FREE_NOWAVES") != nullptr;
+    if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
+    launch_free_split(wl, nwl, nwl_max, rowptr, heavy_deg, f, 0, s);
+    i64 cnt[4];
+    CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 2 * sizeof(i64), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (cnt[1] > 0 && !no_waves) {
+      const auto tw0 = std::chrono::steady_clock::now();
+      const i64 nh = cnt[1];
+      launch_free_heavy(rowptr, col, cur, f.heavy[0], cnt[1], f.light[0], f.cnt, dist, partial, S.fw, s);
+      CUDA_CHECK(cudaMemsetAsync(f.cnt + 1, 0, sizeof(i64), s));
+      CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 2 * sizeof(i64), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      if (trace)
+        std::fprintf(stderr, "[free] heavy waves (%lld vertices) %.1f us, light %lld\n", (long long)nh,
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw0).count(),
+                     (long long)cnt[0]);
+    }
+    for (int it = 0; it < MAX_SWEEPS; it++) {
+      const int p = it & 1, q = p ^ 1;
+      launch_free_iteration(rowptr, col, cur, f, p, cnt[2 * p], cnt[2 * p + 1], it > 0 ? (int)rank_cap : 0,
+                            dist, partial, s);
+      CUDA_CHECK(cudaMemcpyAsync(cnt + 2 * q, S.fcnt.p + 2 * q, 2 * sizeof(i64), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      if (trace)
+        std::fprintf(stderr, "[free] it=%d light %lld -> %lld heavy %lld -> %lld\n", it, (long long)cnt[2 * p],
+                     (long long)cnt[2 * q], (long long)cnt[2 * p + 1], (long long)cnt[2 * q + 1]);
+      if (cnt[2 * q] == 0 && cnt[2 * q + 1] == 0) {
+        if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
+        if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
+        return;
+      }
+    }
+    throw Error(CHROMA_ERUNTIME, "speculative loop failed to settle");
+  }
+  if (algo == CHROMA_ALGO_GAUSS_SEIDEL) {
     GsLaunch L;
     L.rowptr = rowptr;
     L.col = col;
@@ -279,7 +337,9 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     CUDA_CHECK(cudaMemsetAsync(w.stats.p, 0, sizeof(unsigned long long) * nstats, s));
     CUDA_CHECK(cudaEventRecord(ev[0], s));
     // worklist (ordered compaction: ascending local id)
-    k_flag_worklist<<<G(w.NL), 256, 0, s>>>(w.colors.p, w.owned_flag.p, w.NL, round == 0 || gs, w.cs.flags.p);
+    // Jacobi re-colours uncoloured ghosts too (F7); the other modes only owned ones
+    k_flag_worklist<<<G(w.NL), 256, 0, s>>>(w.colors.p, w.owned_flag.p, w.NL,
+                                            round == 0 || algo != CHROMA_ALGO_JACOBI, w.cs.flags.p);
     count_launch();
     select_flagged(w.cs.flags.p, w.NL, w.cs.wl.p, w.cs.nwl.p, s);
     k_count_recolored<<<G(w.NL), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,

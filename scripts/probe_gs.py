@@ -22,7 +22,12 @@ def run(name, g, mode, check=True, reps=3, P=1, algorithm=None):
     if check:
         ow = oracle.World(g.row_offsets, g.col_indices, PT.partition_block(g, P).owner, P, R.ghost_layers_for(R.Mode(mode)))
         ref, _ = ow.run(mode, False, True)
-        ok = "EXACT" if np.array_equal(ref, colors) else "MISMATCH"
+        if algorithm == "free":
+            vm = {"d1": "d1", "d1-2gl": "d1", "d2": "d2", "pd2": "pd2"}[mode]
+            bad = len(oracle.verify(g.row_offsets, g.col_indices, colors, vm))
+            ok = f"{'PROPER' if bad == 0 else f'BAD({bad})'} gs_colors={ref.max()} ratio={colors.max()/max(1,ref.max()):.3f}"
+        else:
+            ok = "EXACT" if np.array_equal(ref, colors) else "MISMATCH"
     print(f"{name:28s} {mode:6s} P={P} n={g.num_vertices:9d} m={len(g.col_indices)//2:10d} build={tb*1e3:8.1f}ms "
           f"total={best[0]*1e3:8.3f}ms kernel={best[1]*1e3:8.3f}ms detect={best[4]*1e3:7.3f}ms rounds={len(reps_)} "
           f"colors={colors.max()} {ok}", flush=True)
@@ -43,3 +48,24 @@ if "jac" in which:
     run("27pt 32^3 jacobi", G.gen_stencil27(32, device="cuda"), "d1-2gl", check=False, algorithm="jacobi")
     run("rmat s18 jacobi P8", G.gen_rmat(18, 16, 1, device="cuda"), "d1", check=False, algorithm="jacobi", P=8)
     run("rmat s18 gs P8", G.gen_rmat(18, 16, 1, device="cuda"), "d1", check=False, P=8)
+if "pd2s" in which:
+    for sc in (16, 18, 20):
+        run(f"pd2 2^{sc} rows", G.gen_random_bipartite(1 << sc, 32, 3, device="cuda").graph, "pd2", check=(sc <= 18))
+if "d2s" in which:
+    run("7pt 100^3 d2", G.gen_hex_mesh(100, 100, 100), "d2")
+    run("7pt 200^3 d2", G.gen_hex_mesh(200, 200, 200), "d2", check=False)
+if "free" in which:
+    run("27pt 128^3 free", G.gen_stencil27(128, device="cuda"), "d1-2gl", algorithm="free")
+    run("27pt 128^3 free P8", G.gen_stencil27(128, device="cuda"), "d1-2gl", algorithm="free", P=8)
+    run("rmat s18 free", G.gen_rmat(18, 16, 1, device="cuda"), "d1", algorithm="free")
+    run("rmat s20 free", G.gen_rmat(20, 16, 1, device="cuda"), "d1", algorithm="free")
+    run("rmat s20 free P8", G.gen_rmat(20, 16, 1, device="cuda"), "d1", algorithm="free", P=8)
+    run("rmat s20 gs P8", G.gen_rmat(20, 16, 1, device="cuda"), "d1", check=False, P=8)
+    run("7pt 100^3 d2 free", G.gen_hex_mesh(100, 100, 100), "d2", algorithm="free")
+    run("pd2 2^18 free", G.gen_random_bipartite(1 << 18, 32, 3, device="cuda").graph, "pd2", algorithm="free")
+    run("pd2 2^20 free", G.gen_random_bipartite(1 << 20, 32, 3, device="cuda").graph, "pd2", algorithm="free", check=False)
+    run("rmat s22 free P8", G.gen_rmat(22, 16, 1, device="cuda"), "d1", algorithm="free", P=8, check=False)
+if "freetrace" in which:
+    run("27pt 128^3 free", G.gen_stencil27(128, device="cuda"), "d1-2gl", algorithm="free", reps=1, check=False)
+    run("rmat s20 free", G.gen_rmat(20, 16, 1, device="cuda"), "d1", algorithm="free", reps=1, check=False)
+    run("pd2 2^18 free", G.gen_random_bipartite(1 << 18, 32, 3, device="cuda").graph, "pd2", algorithm="free", reps=1, check=False)
