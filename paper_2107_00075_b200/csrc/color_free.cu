@@ -24,9 +24,6 @@
 // each.  All passes are HBM/L2-bound gathers.
 #include <cstdio>
 #include <cstdlib>
-#include <thrust/device_ptr.h>
-#include <thrust/execution_policy.h>
-#include <thrust/sort.h>
 
 #include "kernels.cuh"
 
@@ -489,9 +486,7 @@ namespace chroma {
 void launch_free_heavy(const i64* rowptr, const i32* col, i32* colors, i32* heavy, i64 n, i32* light,
                        i64* nlight, int dist, bool partial, FreeWaveScratch& ws, cudaStream_t s) {
   if (n <= 0) return;
-  auto p = thrust::device_pointer_cast(heavy);
-  thrust::sort(thrust::cuda::par.on(s), p, p + n);  // natural (id) order within the core
-  count_launch();
+  sort_i32(heavy, n, s);  // natural (id) order within the core
   const int C = std::min(num_sms(), MAXC);
   ws.F.reserve((i64)C * WWORDS, s);
   ws.A.reserve((i64)C * AWORDS, s);

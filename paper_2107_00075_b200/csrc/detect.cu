@@ -14,6 +14,10 @@
 //   4. fired events uncolour their losers; the count is the number of fired events.
 // In free-running mode (sequential = false) every event fires (classic parallel
 // detection: every conflicting pair loses one endpoint).
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+
 #include "kernels.cuh"
 
 namespace chroma {
@@ -145,16 +149,229 @@ __global__ void __launch_bounds__(1024) k_resolve(const int2* ev, i64 E, uint8_t
   if (t == 0) *conflicts += fired_count;
 }
 
+// Incremental detection: an event (equal non-zero colours on a scanned pair) can
+// only exist if one endpoint changed colour since the previous detection (which
+// left no conflicting pair behind, and unchanged pairs keep their colours).  Mark
+// every vertex within DIST hops of a changed, coloured vertex; the scan then visits
+// only marked rows, in the same order, so the event sequence is unchanged.
+template <int DIST>
+__global__ void k_mark_changed(const i64* rowptr, const i32* col, const i32* colors, const i32* prev, i64 n,
+                               uint8_t* mark) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 b = warp * 32; b < n; b += nwarps * 32) {
+    const i64 i = b + lane;
+    bool ch = false;
+    if (i < n) {
+      const i32 c = colors[i];
+      ch = c != 0 && c != prev[i];
+    }
+    unsigned m = __ballot_sync(FULL, ch);
+    while (m) {
+      const int l = __ffs(m) - 1;
+      m &= m - 1;
+      const i32 v = (i32)(b + l);
+      if (lane == 0) mark[v] = 1;
+      const i64 rs = rowptr[v], re = rowptr[v + 1];
+      if (DIST == 1) {
+        for (i64 e = rs + lane; e < re; e += 32) mark[col[e]] = 1;
+      } else {
+        for (i64 e = rs; e < re; e++) {
+          const i32 u = col[e];
+          if (lane == 0) mark[u] = 1;
+          for (i64 g = rowptr[u] + lane; g < rowptr[u + 1]; g += 32) mark[col[g]] = 1;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_mark_flags(const i32* rows, i64 n, const uint8_t* mark, uint8_t* flags) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    flags[i] = mark[rows[i]];
+}
+
+// ---- free-running D1: pair-centric detection around changed vertices --------
+// Without the reference's ordered replay (every conflicting pair loses its loser),
+// only pairs touching a vertex whose colour changed since the previous detection
+// can conflict.  Each such vertex scans its row; a pair with a ghost end and equal
+// non-zero colours uncolours its loser (degree / gid-hash cascade).  The count is
+// the number of vertices uncoloured (atomicExch makes repeats idempotent).
+constexpr i64 DET_HEAVY = 2048;
+constexpr int DET_HEAVY_THREADS = 512;
+
+__global__ void k_changed_split(const i32* colors, const i32* prev, i64 n, const i64* rowptr, i32* light,
+                                i32* heavy, unsigned long long* cnt) {
+  const int lane = threadIdx.x & 31;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 b = (blockIdx.x * (i64)blockDim.x + threadIdx.x) & ~31ll; b < n; b += stride) {
+    const i64 i = b + lane;
+    bool ch = false, h = false;
+    if (i < n) {
+      const i32 c = colors[i];
+      ch = c != 0 && (prev == nullptr || c != prev[i]);
+      if (ch) h = rowptr[i + 1] - rowptr[i] > DET_HEAVY;
+    }
+    const unsigned mh = __ballot_sync(FULL, ch && h), ml = __ballot_sync(FULL, ch && !h);
+    unsigned long long oh = 0, ol = 0;
+    if (lane == 0) {
+      if (ml) ol = atomicAdd(cnt, (unsigned long long)__popc(ml));
+      if (mh) oh = atomicAdd(cnt + 1, (unsigned long long)__popc(mh));
+    }
+    ol = __shfl_sync(FULL, ol, 0);
+    oh = __shfl_sync(FULL, oh, 0);
+    const unsigned below = lanemask_lt();
+    if (ch && h) heavy[oh + __popc(mh & below)] = (i32)i;
+    else if (ch) light[ol + __popc(ml & below)] = (i32)i;
+  }
+}
+
+struct FreeDet {
+  const i64* rowptr;
+  const i32* col;
+  i32* colors;
+  const uint8_t* owned;
+  const i64* gids;
+  const i32* deg;
+  bool rd;
+};
+
+__device__ __forceinline__ int free_pair(const FreeDet& a, i32 x, bool ox, i32 cx, i32 y) {
+  if (ox && a.owned[y]) return 0;
+  const i32 cy = ld_relaxed(a.colors + y);
+  if (cy != cx) return 0;
+  const i32 loser = v_loses(a.gids[x], a.gids[y], a.deg[x], a.deg[y], a.rd) ? x : y;
+  return atomicExch(a.colors + loser, 0) != 0 ? 1 : 0;
+}
+
+__global__ void k_free_light(FreeDet a, const i32* list, const unsigned long long* n_dev,
+                             unsigned long long* conflicts) {
+  const int lane = threadIdx.x & 31;
+  const i64 n = (i64)*n_dev;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  int mine = 0;
+  for (i64 i = warp; i < n; i += nwarps) {
+    const i32 x = list[i];
+    const bool ox = a.owned[x];
+    const i64 rs = a.rowptr[x], re = a.rowptr[x + 1];
+    for (i64 e = rs + lane; e < re; e += 32) {
+      const i32 cx = ld_relaxed(a.colors + x);
+      if (cx == 0) break;  // already uncoloured by another pair
+      mine += free_pair(a, x, ox, cx, a.col[e]);
+    }
+  }
+  mine = __reduce_add_sync(FULL, mine);
+  if (lane == 0 && mine) atomicAdd(conflicts, (unsigned long long)mine);
+}
+
+__global__ void __launch_bounds__(DET_HEAVY_THREADS) k_free_heavy(FreeDet a, const i32* list,
+                                                                  const unsigned long long* n_dev,
+                                                                  unsigned long long* conflicts) {
+  const int lane = threadIdx.x & 31;
+  const i64 n = (i64)*n_dev;
+  int mine = 0;
+  for (i64 i = blockIdx.x; i < n; i += gridDim.x) {
+    const i32 x = list[i];
+    const bool ox = a.owned[x];
+    const i64 rs = a.rowptr[x], re = a.rowptr[x + 1];
+    for (i64 e = rs + threadIdx.x; e < re; e += DET_HEAVY_THREADS) {
+      const i32 cx = ld_relaxed(a.colors + x);
+      if (cx == 0) break;
+      mine += free_pair(a, x, ox, cx, a.col[e]);
+    }
+  }
+  mine = __reduce_add_sync(FULL, mine);
+  if (lane == 0 && mine) atomicAdd(conflicts, (unsigned long long)mine);
+}
+
 }  // namespace
+
+static void run_detect_free_d1(const DetectArgs& A, i64 nv, DetectScratch& S, unsigned long long* conflicts,
+                               cudaStream_t s) {
+  S.chl.reserve(nv, s);
+  S.chh.reserve(nv, s);
+  S.nch.reserve(2, s);
+  CUDA_CHECK(cudaMemsetAsync(S.nch.p, 0, 2 * sizeof(unsigned long long), s));
+  k_changed_split<<<grid_for(nv, 256, num_sms() * 8), 256, 0, s>>>(
+      A.colors, S.prev_valid ? S.prev.p : nullptr, nv, A.rowptr, S.chl.p, S.chh.p, S.nch.p);
+  FreeDet a{A.rowptr, A.col, A.colors, A.owned_flag, A.gids, A.deg, A.recolor_degrees};
+  k_free_heavy<<<num_sms() * 4, DET_HEAVY_THREADS, 0, s>>>(a, S.chh.p, S.nch.p + 1, conflicts);
+  k_free_light<<<grid_for(nv * 32, 256, num_sms() * 16), 256, 0, s>>>(a, S.chl.p, S.nch.p, conflicts);
+  count_launch(3);
+  CUDA_CHECK(cudaGetLastError());
+  S.prev.reserve(nv, s);
+  CUDA_CHECK(cudaMemcpyAsync(S.prev.p, A.colors, sizeof(i32) * nv, cudaMemcpyDeviceToDevice, s));
+  S.prev_valid = true;
+}
 
 void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
                 unsigned long long* conflicts_dev, cudaStream_t s) {
   if (A.nrows <= 0) return;
+  if (A.incremental && !A.sequential && A.dist == 1 && A.owned_flag) {
+    run_detect_free_d1(A, num_vertices, S, conflicts_dev, s);
+    return;
+  }
+  static const bool trace = std::getenv("CHROMA_DETECT_TRACE") != nullptr;
+  cudaEvent_t te[6];
+  int nte = 0;
+  auto mark_t = [&]() {
+    if (!trace) return;
+    CUDA_CHECK(cudaEventCreate(&te[nte]));
+    CUDA_CHECK(cudaEventRecord(te[nte++], s));
+  };
+  struct Report {
+    std::function<void()> f;
+    ~Report() { f(); }
+  } report{[&]() {
+    if (!trace || nte < 2) return;
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "[detect] rows %lld", (long long)A.nrows);
+    for (int i = 1; i < nte; i++) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, te[i - 1], te[i]);
+      std::fprintf(stderr, " | %.1f us", ms * 1e3);
+    }
+    std::fprintf(stderr, "\n");
+    for (int i = 0; i < nte; i++) cudaEventDestroy(te[i]);
+  }};
+  mark_t();
   DevDetect a{A.rowptr, A.col, A.colors, A.gids, A.deg, A.rows, A.nrows, A.recolor_degrees};
-  S.cnt.reserve(A.nrows, s);
-  S.off.reserve(A.nrows, s);
+  // remember this call's final colours for the next incremental call
+  auto save_prev = [&]() {
+    if (!A.incremental) return;
+    S.prev.reserve(num_vertices, s);
+    CUDA_CHECK(cudaMemcpyAsync(S.prev.p, A.colors, sizeof(i32) * num_vertices, cudaMemcpyDeviceToDevice, s));
+    S.prev_valid = true;
+  };
+  if (A.incremental && S.prev_valid) {
+    S.mark.reserve(num_vertices, s);
+    CUDA_CHECK(cudaMemsetAsync(S.mark.p, 0, num_vertices, s));
+    const int gm = grid_for(num_vertices, 256, num_sms() * 16);
+    if (A.dist == 1) k_mark_changed<1><<<gm, 256, 0, s>>>(A.rowptr, A.col, A.colors, S.prev.p, num_vertices, S.mark.p);
+    else k_mark_changed<2><<<gm, 256, 0, s>>>(A.rowptr, A.col, A.colors, S.prev.p, num_vertices, S.mark.p);
+    count_launch();
+    S.arows.reserve(A.nrows, s);
+    S.narows.reserve(1, s);
+    // row flags reuse the fired buffer (sized later for events)
+    S.fired.reserve(A.nrows, s);
+    k_mark_flags<<<grid_for(A.nrows, 256, num_sms() * 16), 256, 0, s>>>(A.rows, A.nrows, S.mark.p, S.fired.p);
+    count_launch();
+    select_flagged_values(A.rows, S.fired.p, A.nrows, S.arows.p, S.narows.p, s);
+    mark_t();
+    i64 na = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&na, S.narows.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (na == 0) return;  // nothing changed: colours equal prev already
+    a.rows = S.arows.p;
+    a.nrows = na;
+  }
+  const i64 nrows = a.nrows;
+  S.cnt.reserve(nrows, s);
+  S.off.reserve(nrows, s);
   S.total.reserve(1, s);
-  const int g = grid_for(A.nrows * 32, 256, num_sms() * 16);
+  const int g = grid_for(nrows * 32, 256, num_sms() * 16);
   auto launch = [&](auto wr) {
     constexpr bool W = decltype(wr)::value;
     if (A.dist == 1) k_events<1, false, W><<<g, 256, 0, s>>>(a, S.cnt.p, S.off.p, S.ev.p);
@@ -164,21 +381,29 @@ void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
     CUDA_CHECK(cudaGetLastError());
   };
   launch(std::false_type{});
-  exclusive_scan_i64(S.cnt.p, S.off.p, A.nrows, s);
-  k_total<<<1, 1, 0, s>>>(S.cnt.p, S.off.p, A.nrows, S.total.p);
+  exclusive_scan_i64(S.cnt.p, S.off.p, nrows, s);
+  k_total<<<1, 1, 0, s>>>(S.cnt.p, S.off.p, nrows, S.total.p);
   count_launch();
+  mark_t();
   i64 E = 0;
   CUDA_CHECK(cudaMemcpyAsync(&E, S.total.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
-  if (E == 0) return;
+  if (E == 0) {
+    save_prev();
+    return;
+  }
   CHROMA_REQUIRE(E < INT32_MAX, CHROMA_ERUNTIME, "too many conflict events");
   S.ev.reserve(E, s);
   launch(std::true_type{});
+  mark_t();
   S.fired.reserve(E, s);
   S.kill.reserve(num_vertices, s);
   k_resolve<<<1, 1024, 0, s>>>(S.ev.p, E, S.fired.p, S.kill.p, A.colors, conflicts_dev, A.sequential);
   count_launch();
   CUDA_CHECK(cudaGetLastError());
+  mark_t();
+  save_prev();
+  mark_t();
 }
 
 }  // namespace chroma

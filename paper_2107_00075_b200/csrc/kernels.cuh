@@ -74,6 +74,7 @@ void select_flagged(const uint8_t* flags, i64 n, i32* out, i64* n_out, cudaStrea
 void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* out, i64* n_out,
                            cudaStream_t s);
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s);
+void sort_i32(i32* keys, i64 n, cudaStream_t s);  // ascending, in place (non-negative keys)
 
 // ---------------------------------------------------------------- detection
 struct DetectArgs {
@@ -88,6 +89,9 @@ struct DetectArgs {
   bool partial;
   bool recolor_degrees;
   bool sequential;    // exact replay of the reference's in-place scan (F5)
+  bool incremental = false;  // scan only rows near vertices whose colour changed since
+                             // the previous incremental call (S.prev)
+  const uint8_t* owned_flag = nullptr;  // D1 free-running fast path: pairs with a ghost end
 };
 struct DetectScratch {
   DBuf<i64> cnt, off;
@@ -96,6 +100,13 @@ struct DetectScratch {
   DBuf<i32> kill;
   DBuf<unsigned long long> result;  // [0] conflicts
   DBuf<i64> total;
+  // incremental mode: colours at the end of the previous detection, row marks
+  DBuf<i32> prev, arows;
+  DBuf<uint8_t> mark;
+  DBuf<i64> narows;
+  DBuf<i32> chl, chh;  // changed vertices, light / heavy rows (free-running D1)
+  DBuf<unsigned long long> nch;
+  bool prev_valid = false;
 };
 // Adds the number of conflicts to *conflicts_dev (device, unsigned long long).
 void run_detect(const DetectArgs& a, i64 num_vertices, DetectScratch& S,

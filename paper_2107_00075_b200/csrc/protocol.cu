@@ -109,15 +109,11 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     nwl_max = k;
   }
   if (algo == CHROMA_ALGO_FREE) {
-    // color_free.cu: in-place first fit -> larger id keeps its colour -> the losers
-    // iterate with snapshot rank-offset first fit until none is left
-    i32* cur = colors;
-    if (!colors_nonneg) {
-      S.val.reserve(nv, s);
-      launch_clamp_nonneg(S.val.p, colors, nv, s);
-      cur = S.val.p;
-    }
-    launch_scatter_const(cur, wl, nwl, nwl_max, 0, s);
+    // color_free.cu: exact waves over heavy rows, then in-place first fit over the
+    // light ones -> larger id keeps its colour -> the losers iterate until none is
+    // left.  A distance-1 worklist without heavy rows (meshes, later rounds) has no
+    // dense core to speculate around: it takes the ordered dataflow kernel instead,
+    // which is conflict-free and uses the reference's colour count.
     for (auto& b : S.fl) b.reserve(nwl_max, s);
     S.fcnt.reserve(4, s);
     FreeLists f{{S.fl[0].p, S.fl[1].p}, {S.fl[2].p, S.fl[3].p}, S.fcnt.p};
@@ -125,11 +121,24 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     static const i64 rank_cap = env_i64("CHROMA_FREE_RANKCAP", 0);
     static const bool trace = std::getenv("CHROMA_FREE_TRACE") != nullptr;
     static const bool no_waves = std::getenv("CHROMA_FREE_NOWAVES") != nullptr;
+    static const bool always_spec = std::getenv("CHROMA_FREE_SPECULATE") != nullptr;
     if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
     launch_free_split(wl, nwl, nwl_max, rowptr, heavy_deg, f, 0, s);
     i64 cnt[4];
     CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 2 * sizeof(i64), cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
+    if (dist == 1 && cnt[1] == 0 && !always_spec) {
+      algo = CHROMA_ALGO_GAUSS_SEIDEL;
+      goto gauss_seidel;
+    }
+    {
+    i32* cur = colors;
+    if (!colors_nonneg) {
+      S.val.reserve(nv, s);
+      launch_clamp_nonneg(S.val.p, colors, nv, s);
+      cur = S.val.p;
+    }
+    launch_scatter_const(cur, wl, nwl, nwl_max, 0, s);
     if (cnt[1] > 0 && !no_waves) {
       const auto tw0 = std::chrono::steady_clock::now();
       const i64 nh = cnt[1];
@@ -158,7 +167,9 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
       }
     }
     throw Error(CHROMA_ERUNTIME, "speculative loop failed to settle");
+    }
   }
+gauss_seidel:
   if (algo == CHROMA_ALGO_GAUSS_SEIDEL) {
     GsLaunch L;
     L.rowptr = rowptr;
@@ -324,6 +335,9 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   da.partial = partial;
   da.recolor_degrees = rd;
   da.sequential = algo != CHROMA_ALGO_FREE;
+  da.incremental = true;
+  da.owned_flag = w.owned_flag.p;
+  w.det.prev_valid = false;
   const bool remote = w.connected && w.P > 1;
   for (;;) {
     if (round > max_rounds) {

@@ -138,6 +138,20 @@ void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* 
   count_launch();
 }
 
+void sort_i32(i32* keys, i64 n, cudaStream_t s) {
+  if (n <= 1) return;
+  static thread_local DBuf<i32>* alt = new DBuf<i32>();
+  alt->reserve(n, s);
+  cub::DoubleBuffer<i32> db(keys, alt->p);
+  size_t bytes = 0;
+  CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, (int)n, 0, 32, s));
+  t_cub_tmp.reserve((i64)bytes, s);
+  CUDA_CHECK(cub::DeviceRadixSort::SortKeys(t_cub_tmp.p, bytes, db, (int)n, 0, 32, s));
+  count_launch();
+  if (db.Current() != keys)
+    CUDA_CHECK(cudaMemcpyAsync(keys, db.Current(), sizeof(i32) * n, cudaMemcpyDeviceToDevice, s));
+}
+
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s) {
   if (n <= 0) return;
   size_t bytes = 0;

@@ -69,3 +69,14 @@ if "freetrace" in which:
     run("27pt 128^3 free", G.gen_stencil27(128, device="cuda"), "d1-2gl", algorithm="free", reps=1, check=False)
     run("rmat s20 free", G.gen_rmat(20, 16, 1, device="cuda"), "d1", algorithm="free", reps=1, check=False)
     run("pd2 2^18 free", G.gen_random_bipartite(1 << 18, 32, 3, device="cuda").graph, "pd2", algorithm="free", reps=1, check=False)
+if "rounds" in which:
+    g = G.gen_rmat(20, 16, 1, device="cuda")
+    for alg in ("free", None):
+        w = RT.build_local_graphs(g, PT.partition_block(g, 8), 1)
+        cfg = R.AlgorithmConfig(mode=R.Mode("d1"), deterministic=alg is None, algorithm=alg)
+        colors, reps_ = R.run_distributed(w, cfg)
+        colors, reps_ = R.run_distributed(w, cfg)
+        print("algorithm", alg)
+        for r in reps_:
+            print(f"  round {r.round_index:3d} conflicts={r.conflicts:7d} recolored={sum(r.recolored_per_rank):8d} "
+                  f"color={r.time_color_s*1e3:7.3f}ms comm={r.time_comm_s*1e3:7.3f}ms detect={r.time_detect_s*1e3:7.3f}ms")
