@@ -1,13 +1,17 @@
 #!/usr/bin/env python
 """Benchmark: distributed speculate-and-iterate colouring on B200 (BASELINE.json metric).
 
-Workload (configs[1], "C2"): D1-2GL colouring of the 3-D 27-point stencil mesh 128^3
-(2,097,152 vertices, 26,822,908 undirected edges), partition_block over P = N ranks,
-one rank per GPU, deterministic mode (bit-exact with the reference).  One step = one
-full run_distributed (every round: colour, halo exchange over NVLink, detection,
+Default workload (configs[1], "C2"): D1-2GL colouring of the 3-D 27-point stencil mesh
+128^3 (2,097,152 vertices, 26,822,908 undirected edges), partition_block over P = N
+ranks, one rank per GPU, deterministic mode (bit-exact with the reference).  One step =
+one full run_distributed (every round: colour, halo exchange over NVLink, detection,
 allreduce) on the device-resident world.
 
+"--workload c3" runs configs[2], the north-star target: D1 colouring of the permuted
+R-MAT scale-24 graph (edge factor 16), P = N, free-running mode by default.
+
     python bench.py [--gpus N --steps K --warmup W]            # our B200 path
+    python bench.py --workload c3 [--scale 24] [...]            # R-MAT (north-star target)
     python bench.py --impl reference [...]                      # reference arm (CPU)
     torchrun --nproc-per-node N bench.py --gpus N ...           # N > 1
 
@@ -29,8 +33,37 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-METRIC = "coloring edges/s (D1-2GL, 27-pt stencil 128^3)"
 UNIT = "edges/s"
+
+
+class Workload:
+    """The benchmarked configuration (BASELINE.json configs[1] or configs[2])."""
+
+    def __init__(self, args):
+        self.name = args.workload
+        if self.name == "c2":
+            self.mode, self.gl, self.vmode = "d1-2gl", 2, "d1"
+            self.metric = f"coloring edges/s (D1-2GL, 27-pt stencil {args.L}^3)"
+            self.algorithm = args.algorithm or "gauss-seidel"
+            self.desc = f"C2: D1-2GL 27-point stencil {args.L}^3"
+            self.data = "synthetic (27-point stencil generated on device, id = x + L(y + L z))"
+        else:
+            self.mode, self.gl, self.vmode = "d1", 1, "d1"
+            self.metric = f"coloring edges/s (D1, R-MAT scale-{args.scale} ef16)"
+            self.algorithm = args.algorithm or "free"
+            self.desc = f"C3: D1 R-MAT scale-{args.scale} edge factor 16 (permuted)"
+            self.data = "synthetic (Graph500 R-MAT a=.57 b=c=.19, seeded label permutation, generated on device)"
+        self.args = args
+
+    def graph(self, device=None, scale=None):
+        from paper_2107_00075_b200 import graph as G
+        if self.name == "c2":
+            return G.gen_stencil27(self.args.L, device=device)
+        return G.gen_rmat(scale or self.args.scale, 16, 1, device=device)
+
+    def sample_scale(self) -> int:
+        """Bounded CPU sample for the C3 oracle timing (the full graph takes hours in Python)."""
+        return min(self.args.scale, 18)
 
 
 _JSON_FD = None
@@ -61,8 +94,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--L", type=int, default=128, help="stencil edge length (128 = BASELINE config)")
-    ap.add_argument("--algorithm", default="gauss-seidel", choices=["gauss-seidel", "free", "jacobi"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--L", type=int, default=128, help="C2 stencil edge length (128 = BASELINE config)")
+    ap.add_argument("--scale", type=int, default=24, help="C3 R-MAT scale (24 = BASELINE config)")
+    ap.add_argument("--algorithm", default=None, choices=["gauss-seidel", "free", "jacobi"],
+                    help="default: gauss-seidel (deterministic, bit-exact) for c2, free for c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -124,36 +160,33 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def c2_graph(L: int, device=None):
-    from paper_2107_00075_b200 import graph as G
-    return G.gen_stencil27(L, device=device)
-
-
 def round0_bytes(n_owned: int, nnz_owned: int, touched: int) -> int:
     """Algorithmic bytes of one round-0 colouring launch: colour write,
     row pointers (int64 pair per row), int32 column indices, distinct colours read."""
     return 4 * n_owned + 8 * (n_owned + 1) + 4 * nnz_owned + 4 * touched
 
 
-def cpu_baseline(L: int, P: int, budget_s: float = 30.0) -> dict:
+def cpu_baseline(wl: "Workload", P: int, budget_s: float = 30.0) -> dict:
     """The C oracle (port of the reference path) on the host, single thread."""
     import oracle
     from paper_2107_00075_b200 import partition as PT
-    g = c2_graph(L)
+    g = wl.graph(scale=wl.sample_scale() if wl.name == "c3" else None)
     pm = PT.partition_block(g, P)
-    w = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, 2)
+    w = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, wl.gl)
     t0 = time.perf_counter()
     reps = 0
     while True:
-        w.run("d1-2gl", False, True)
+        w.run(wl.mode, False, True)
         reps += 1
         el = time.perf_counter() - t0
         if el > budget_s / 3 or reps >= 3:
             break
     sec = el / reps
     m = len(g.col_indices) // 2
+    what = (f"the full 27-pt {wl.args.L}^3 mesh" if wl.name == "c2"
+            else f"R-MAT scale-{wl.sample_scale()} (bounded sample of the scale-{wl.args.scale} workload)")
     return {"value": m / sec, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"oracle run_distributed (D1-2GL deterministic) on the full 27-pt {L}^3 mesh, "
+            "sample": f"oracle run_distributed ({wl.mode}, deterministic) on {what}, "
                       f"P={P}, {reps} rep(s), {sec:.3f} s/step, 1 of {os.cpu_count()} cores"}
 
 
@@ -164,29 +197,33 @@ def run_reference(args):
         return
     import oracle
     from paper_2107_00075_b200 import partition as PT
+    wl = Workload(args)
     P = args.gpus
-    g = c2_graph(args.L)
+    g = wl.graph(scale=wl.sample_scale() if wl.name == "c3" else None)
     pm = PT.partition_block(g, P)
-    w = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, 2)
+    w = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, wl.gl)
     for _ in range(args.warmup):
-        w.run("d1-2gl", False, True)
+        w.run(wl.mode, False, True)
     t = []
     colors = None
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        colors, reps = w.run("d1-2gl", False, True)
+        colors, reps = w.run(wl.mode, False, True)
         t.append(time.perf_counter() - t0)
     m = len(g.col_indices) // 2
     T = sum(t)
     val = m * args.steps / T
     ncol = int(len(np.unique(colors[colors > 0])))
-    line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": P, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"C2: D1-2GL 27-point stencil {args.L}^3, partition_block P={P}, deterministic",
+    sample = ("full workload each step" if wl.name == "c2"
+              else f"R-MAT scale-{wl.sample_scale()} each step (bounded sample of scale {args.scale})")
+    line = {"metric": wl.metric, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": P,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": f"{wl.desc}, partition_block P={P}, deterministic (oracle)",
                        "n": g.num_vertices, "m": m, "rounds": len(reps), "colors": ncol},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": f"oracle/ C port of the reference path, full workload each step, "
+                             "sample": f"oracle/ C port of the reference path, {sample}, "
                                        f"1 of {os.cpu_count()} cores"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
@@ -230,22 +267,26 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    g = c2_graph(args.L, device=f"cuda:{local}")
+    wl = Workload(args)
+    g = wl.graph(device=f"cuda:{local}")
     m = len(g.col_indices) // 2
     pm = PT.partition_block(g, N)
-    cfg = R.AlgorithmConfig(mode=R.Mode.D1_2GL, deterministic=args.algorithm == "gauss-seidel",
-                            algorithm=None if args.algorithm == "gauss-seidel" else args.algorithm)
+    cfg = R.AlgorithmConfig(mode=R.Mode(wl.mode), deterministic=wl.algorithm == "gauss-seidel",
+                            algorithm=None if wl.algorithm == "gauss-seidel" else wl.algorithm)
 
     def make_world():
         if N == 1:
-            return RT.build_local_graphs(g, pm, 2)
+            return RT.build_local_graphs(g, pm, wl.gl)
         from paper_2107_00075_b200.dist import DistWorld
-        return DistWorld(g, pm, 2)
+        return DistWorld(g, pm, wl.gl)
 
     world = make_world()
     lg = world.local_graphs[0] if N == 1 else world.local_graph
+    # `value` keeps the result in HBM (device output); e2e below returns it to the host
+    n_out = world.output_length() if hasattr(world, "output_length") else world.num_global_vertices
+    out = torch.empty(n_out, dtype=torch.int32, device=f"cuda:{local}")
     for _ in range(args.warmup):
-        R.run_distributed(world, cfg)
+        R.run_distributed(world, cfg, out=out)
 
     import ctypes as C
     tbuf = (C.c_double * 5)()
@@ -255,14 +296,16 @@ def main():
     l0 = launch_count()
     per = []
     kern = []
+    r0 = []
     rounds = 0
     colors = None
     for _ in range(args.steps):
         barrier()
-        colors, reports = R.run_distributed(world, cfg)
+        colors, reports = R.run_distributed(world, cfg, out=out)
         _lib.check(_lib.lib().chroma_world_last_timing(world.handle.h, tbuf))
         per.append(tbuf[0])
         kern.append(tbuf[1])
+        r0.append(reports[0].time_color_s)
         rounds = len(reports)
     torch.cuda.synchronize()
     barrier()
@@ -272,6 +315,7 @@ def main():
     TK = allmax(sum(kern))
     value = m * args.steps / T
     # ---- colour count and properness (global, after timing)
+    colors = colors.cpu().numpy()
     if N == 1:
         gcol = colors
     else:
@@ -282,17 +326,20 @@ def main():
         dist.all_gather(bufs, own)
         gcol = torch.cat(bufs).cpu().numpy()  # partition_block: owned ranges are contiguous in gid order
     ncol, _ = V.color_stats(gcol) if rank == 0 else (None, None)
-    nviol = V.count_violations(g, gcol, "d1") if rank == 0 else None
-    # ---- roofline of the dominant kernel (GS colouring, round 0 bytes)
+    nviol = V.count_violations(g, gcol, wl.vmode) if rank == 0 else None
+    # ---- roofline of the dominant kernel (colouring, round 0 bytes)
     n_o = lg.owned_count
     nnz_o = int(lg.row_offsets[n_o]) if N > 1 else len(g.col_indices)
     touched = lg.num_local if N > 1 else g.num_vertices
     B = round0_bytes(n_o, nnz_o, touched)
     kernel_s = TK / args.steps
+    if wl.algorithm == "free":
+        # free mode: round 0's colour phase (heavy waves + light speculation) is the unit
+        kernel_s = allmax(sum(r0)) / args.steps
     peak, peak_kind = peaks()
     achieved = B / kernel_s / 1e9
     traffic = None
-    if N == 1 and args.L == 128 and args.algorithm == "gauss-seidel":
+    if N == 1 and wl.name == "c2" and args.L == 128 and wl.algorithm == "gauss-seidel":
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
                 traffic = json.load(fh)["gs_kernel_c2_p1"]["dram_bytes_per_launch"]
@@ -313,10 +360,10 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             if N == 1:
-                wv = RT.build_local_graphs(hg, hpm, 2)
+                wv = RT.build_local_graphs(hg, hpm, wl.gl)
             else:
                 from paper_2107_00075_b200.dist import DistWorld
-                wv = DistWorld(hg, hpm, 2)
+                wv = DistWorld(hg, hpm, wl.gl)
             out, _ = R.run_distributed(wv, cfg)
             torch.cuda.synchronize()
             el = time.perf_counter() - t0
@@ -330,19 +377,19 @@ def main():
                "timing": "host perf_counter around build_local_graphs + run_distributed (synchronous API)"}
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.L, N)
+        cpu = cpu_baseline(wl, N)
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+        line = {"metric": wl.metric, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-                "data": "synthetic (27-point stencil generated on device, id = x + L(y + L z))",
-                "config": {"workload": f"C2: D1-2GL 27-point stencil {args.L}^3, partition_block P={N}, "
-                                       f"{args.algorithm}",
-                           "n": g.num_vertices, "m": m, "ghost_layers": 2, "rounds": rounds, "colors": ncol,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": wl.data,
+                "config": {"workload": f"{wl.desc}, partition_block P={N}, {wl.algorithm}",
+                           "n": g.num_vertices, "m": m, "ghost_layers": wl.gl, "rounds": rounds, "colors": ncol,
                            "violations": nviol, "parallelism": f"vertex-range x{N}",
                            "l2": f"inputs larger than L2 (int32 col {4 * len(g.col_indices) / 1e6:.0f} MB)"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": traffic, "kernel": "gs_kernel (colouring)",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "kernel": ("gs_d1_kernel (colouring)" if wl.algorithm == "gauss-seidel"
+                                        else "round-0 colour phase"),
                              "algorithmic_bytes_per_launch": B, "kernel_ms": kernel_s * 1e3,
                              "peak_kind": peak_kind},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}

@@ -304,6 +304,23 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nb) {
   __syncthreads();
 }
 
+// First colour (1-based) free of row | extra over the WWORDS*32-colour mask, warp-wide;
+// 0 if none.
+__device__ __forceinline__ int first_free(const u32* row, const u32* extra, int lane) {
+#pragma unroll
+  for (int h = 0; h < WWORDS / 32; h++) {
+    const int w = h * 32 + lane;
+    const u32 fr = ~(row[w] | (extra ? extra[w] : 0u));
+    const u32 bl = __ballot_sync(FULL, fr != 0);
+    if (bl) {
+      const int L = __ffs(bl) - 1;
+      const u32 frL = __shfl_sync(FULL, fr, L);
+      return (h * 32 + L) * 32 + __ffs(frL);
+    }
+  }
+  return 0;
+}
+
 template <int DIST, bool PARTIAL>
 __global__ void __launch_bounds__(HEAVY_THREADS, 1)
     k_heavy_waves(const i64* rowptr, const i32* col, i32* colors, const i32* heavy, i64 n, u32* gF, u32* gA,
@@ -313,9 +330,11 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 1)
   __shared__ int sOvf;
   __shared__ u32 sW[MAXC][WWORDS + 1];  // +1: rows start in different banks
   __shared__ i32 sV[MAXC], sC[MAXC];
+  __shared__ u32 sX[WWORDS];
   __shared__ u32 sAdj[MAXC * AWORDS];
   __shared__ int sOv[MAXC];
   const int b = blockIdx.x, C = gridDim.x, t = threadIdx.x, lane = t & 31;
+  if (t < WWORDS) sX[t] = 0;
   if (t == 0 && b < n) st_relaxed(colors + heavy[b], -(b + 1));
   grid_barrier(bar, C);
   for (i64 base = 0; base < n; base += C) {
@@ -383,48 +402,59 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 1)
       for (int i = t; i < m; i += blockDim.x) sOv[i] = __ldcg(gOvf + i), sV[i] = heavy[base + i];
       __syncthreads();
       if (t == 0 && gDbg) atomicAdd((unsigned long long*)(gDbg + 4), (unsigned long long)(gtime() - t2));
-      if (t < 32) {
-        const long long c0 = clock64();
+      // (a) provisional first fit of every member against its row mask, one warp each
+      const int warp = t >> 5, nwarp = blockDim.x >> 5;
+      const long long c0 = clock64();
+      for (int j = warp; j < m; j += nwarp) {
+        const int c = sOv[j] ? 0 : first_free(sW[j], nullptr, lane);
+        if (lane == 0) sC[j] = c;
+      }
+      __syncthreads();
+      // (b) ordered repair: member j keeps its pick unless an earlier adjacent member
+      // holds that colour; then it takes the first colour free of both.  Either way
+      // the result equals the sequential first fit in slot order.
+      if (warp == 0) {
         for (int j = 0; j < m; j++) {
-          int c = 0;
-          if (!sOv[j]) {
-            for (int h = 0; h < WWORDS / 32 && !c; h++) {
-              const int w = h * 32 + lane;
-              const u32 fr = ~sW[j][w];
-              const u32 bl = __ballot_sync(FULL, fr != 0);
-              if (bl) {
-                const int L = __ffs(bl) - 1;
-                const u32 frL = __shfl_sync(FULL, fr, L);
-                c = (h * 32 + L) * 32 + __ffs(frL);
-              }
-            }
-          }
-          if (lane == 0) sC[j] = c;
-          if (c) {
-            // lane l owns members l, l+32, ...: independent updates, no loop-carried chain
-            const int o = c - 1;
-            u32 adj[AWORDS];
+          const int cj = sC[j];
+          if (cj == 0) continue;  // beyond the mask: constrains no one, finished later
+          u32 adj[AWORDS];
 #pragma unroll
-            for (int q = 0; q < AWORDS; q++) adj[q] = sAdj[j * AWORDS + q];
+          for (int q = 0; q < AWORDS; q++) adj[q] = sAdj[j * AWORDS + q];
+          bool clash = false;
+#pragma unroll
+          for (int q = 0; q < AWORDS; q++) {
+            const int k = q * 32 + lane;
+            if (k < j && (adj[q] >> lane & 1) && sC[k] == cj) clash = true;
+          }
+          if (__any_sync(FULL, clash)) {
 #pragma unroll
             for (int q = 0; q < AWORDS; q++) {
               const int k = q * 32 + lane;
-              if (k > j && k < m && (adj[q] >> lane & 1)) sW[k][o >> 5] |= 1u << (o & 31);
+              if (k < j && (adj[q] >> lane & 1)) {
+                const int o = sC[k] - 1;
+                if (o >= 0 && o < WWORDS * 32) atomicOr(&sX[o >> 5], 1u << (o & 31));
+              }
             }
+            __syncwarp();
+            const int c = first_free(sW[j], sX, lane);
+            __syncwarp();
+            sX[lane] = 0;
+            sX[lane + 32] = 0;
+            if (lane == 0) sC[j] = c;
+            __syncwarp();
           }
-          __syncwarp();
         }
-        const long long c1 = clock64();
-        __syncwarp();
-        for (int j = lane; j < m; j += 32) {
-          const i32 v = sV[j], c = sC[j];
-          st_relaxed(colors + v, c);
-          if (!c) light[atomicAdd(nlight, 1ull)] = v;  // beyond the mask: finish it speculatively
-        }
-        if (t == 0 && gDbg) {
-          atomicAdd((unsigned long long*)(gDbg + 5), (unsigned long long)(c1 - c0));
-          atomicAdd((unsigned long long*)(gDbg + 6), (unsigned long long)m);
-        }
+      }
+      const long long c1 = clock64();
+      __syncthreads();
+      for (int j = t; j < m; j += blockDim.x) {
+        const i32 v = sV[j], c = sC[j];
+        st_relaxed(colors + v, c);
+        if (!c) light[atomicAdd(nlight, 1ull)] = v;  // beyond the mask: finish it speculatively
+      }
+      if (t == 0 && gDbg) {
+        atomicAdd((unsigned long long*)(gDbg + 5), (unsigned long long)(c1 - c0));
+        atomicAdd((unsigned long long*)(gDbg + 6), (unsigned long long)m);
       }
     }
     if (b == 0 && t == 0 && gDbg) { atomicAdd((unsigned long long*)(gDbg + 0), (unsigned long long)(t1 - t0)); atomicAdd((unsigned long long*)(gDbg + 2), (unsigned long long)(gtime() - t2)); }
@@ -433,6 +463,18 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 1)
     grid_barrier(bar, C);
     if (b == 0 && t == 0 && gDbg) { const u64 tn = gtime(); atomicAdd((unsigned long long*)(gDbg + 3), (unsigned long long)(tn - t3)); }
   }
+}
+
+__global__ void k_degree_keys(const i32* v, i64 n, const i64* rowptr, u64* keys) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 x = v[i];
+    const u64 d = (u64)(rowptr[x + 1] - rowptr[x]);
+    keys[i] = ((u64)(0xffffffffu - (u32)(d > 0xffffffffull ? 0xffffffffull : d)) << 32) | (u32)x;
+  }
+}
+__global__ void k_unkey(const u64* keys, i64 n, i32* v) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    v[i] = (i32)(keys[i] & 0xffffffffull);
 }
 
 #define FREE_DISPATCH(KERNEL, GRID, BLOCK, ...)                                              \
@@ -486,7 +528,13 @@ namespace chroma {
 void launch_free_heavy(const i64* rowptr, const i32* col, i32* colors, i32* heavy, i64 n, i32* light,
                        i64* nlight, int dist, bool partial, FreeWaveScratch& ws, cudaStream_t s) {
   if (n <= 0) return;
-  sort_i32(heavy, n, s);  // natural (id) order within the core
+  // largest degree first (ties by id): balances the waves' row scans and is the
+  // classic LDF order for the dense core
+  ws.keys.reserve(n, s);
+  k_degree_keys<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(heavy, n, rowptr, ws.keys.p);
+  sort_u64(ws.keys.p, n, s);
+  k_unkey<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(ws.keys.p, n, heavy);
+  count_launch(2);
   const int C = std::min(num_sms(), MAXC);
   ws.F.reserve((i64)C * WWORDS, s);
   ws.A.reserve((i64)C * AWORDS, s);

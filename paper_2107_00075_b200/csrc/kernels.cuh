@@ -48,6 +48,7 @@ struct FreeWaveScratch {
   DBuf<int> ovf;
   DBuf<unsigned> bar;
   DBuf<u64> dbg;
+  DBuf<u64> keys;
 };
 // Exact wave colouring of the heavy list (sorted in place); vertices whose colour
 // would exceed the heavy mask are appended to light[*nlight].
@@ -75,6 +76,7 @@ void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* 
                            cudaStream_t s);
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s);
 void sort_i32(i32* keys, i64 n, cudaStream_t s);  // ascending, in place (non-negative keys)
+void sort_u64(u64* keys, i64 n, cudaStream_t s);  // ascending, in place
 
 // ---------------------------------------------------------------- detection
 struct DetectArgs {

@@ -152,6 +152,20 @@ void sort_i32(i32* keys, i64 n, cudaStream_t s) {
     CUDA_CHECK(cudaMemcpyAsync(keys, db.Current(), sizeof(i32) * n, cudaMemcpyDeviceToDevice, s));
 }
 
+void sort_u64(u64* keys, i64 n, cudaStream_t s) {
+  if (n <= 1) return;
+  static thread_local DBuf<u64>* alt = new DBuf<u64>();
+  alt->reserve(n, s);
+  cub::DoubleBuffer<u64> db(keys, alt->p);
+  size_t bytes = 0;
+  CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, (int)n, 0, 64, s));
+  t_cub_tmp.reserve((i64)bytes, s);
+  CUDA_CHECK(cub::DeviceRadixSort::SortKeys(t_cub_tmp.p, bytes, db, (int)n, 0, 64, s));
+  count_launch();
+  if (db.Current() != keys)
+    CUDA_CHECK(cudaMemcpyAsync(keys, db.Current(), sizeof(u64) * n, cudaMemcpyDeviceToDevice, s));
+}
+
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s) {
   if (n <= 0) return;
   size_t bytes = 0;

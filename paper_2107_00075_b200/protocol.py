@@ -160,11 +160,13 @@ def _reports_from(rep, rec, n, P) -> list:
                         time_detect_s=float(rep[i].time_detect_s)) for i in range(n)]
 
 
-def run_distributed(world, cfg: AlgorithmConfig):
+def run_distributed(world, cfg: AlgorithmConfig, out=None):
     """Speculate-and-iterate driver for all four modes (chroma/protocol.py:263-334).
 
     Returns (int32[num_global_vertices] colours, list[RoundReport]) for a RankWorld;
     for a dist.DistWorld (one rank per process) the colours are this rank's owned slice.
+    ``out`` (extension): a contiguous int32 CUDA tensor of that length on the world's
+    device; the colours are written there (no device-to-host copy) and it is returned.
     """
     mode = Mode(cfg.mode)
     needed = ghost_layers_for(mode)
@@ -179,11 +181,18 @@ def run_distributed(world, cfg: AlgorithmConfig):
     rec = np.zeros((cap, P), dtype=np.int64)
     nrep = C.c_int64(0)
     n_out = world.output_length() if hasattr(world, "output_length") else world.num_global_vertices
-    colors = np.zeros(n_out, dtype=np.int32)
+    if out is not None:
+        if (not getattr(out, "is_cuda", False) or str(out.dtype) != "torch.int32" or not out.is_contiguous()
+                or out.numel() != n_out):
+            raise ValueError(f"out must be a contiguous int32 CUDA tensor of {n_out} elements")
+        colors, optr, flags = out, C.c_void_p(out.data_ptr()), 1
+    else:
+        colors = np.zeros(n_out, dtype=np.int32)
+        optr, flags = _lib.ptr(colors), 0
     st = _lib.lib().chroma_run_distributed(world.handle.h, _lib.MODE[mode.value],
                                            int(bool(cfg.recolor_degrees)), cfg.algo_code(),
-                                           int(cfg.max_rounds), _lib.ptr(colors), rep, _lib.ptr(rec),
-                                           cap, C.byref(nrep), 0)
+                                           int(cfg.max_rounds), optr, rep, _lib.ptr(rec),
+                                           cap, C.byref(nrep), flags)
     reports = _reports_from(rep, rec, nrep.value, P)
     world.total_bytes = sum(r.bytes_sent for r in reports)
     world.total_messages = sum(r.messages_sent for r in reports)

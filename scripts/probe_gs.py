@@ -80,3 +80,9 @@ if "rounds" in which:
         for r in reps_:
             print(f"  round {r.round_index:3d} conflicts={r.conflicts:7d} recolored={sum(r.recolored_per_rank):8d} "
                   f"color={r.time_color_s*1e3:7.3f}ms comm={r.time_comm_s*1e3:7.3f}ms detect={r.time_detect_s*1e3:7.3f}ms")
+if "c3trace" in which:
+    sc = int(os.environ.get("SCALE", "24"))
+    g = G.gen_rmat(sc, 16, 1, device="cuda")
+    print("max degree", int(np.diff(g.row_offsets).max()), "heavy>1024", int((np.diff(g.row_offsets) > 1024).sum()),
+          ">4096", int((np.diff(g.row_offsets) > 4096).sum()), flush=True)
+    run(f"rmat s{sc} free", g, "d1", algorithm="free", check=False, reps=2)
