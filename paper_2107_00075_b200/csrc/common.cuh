@@ -50,6 +50,7 @@ struct DBuf {
   T* p = nullptr;
   i64 n = 0;
   cudaStream_t s = nullptr;
+  bool borrowed = false;  // p belongs to someone else (e.g. an IPC-shared region)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
@@ -57,23 +58,31 @@ struct DBuf {
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; n = o.n; s = o.s;
-      o.p = nullptr; o.n = 0;
+      p = o.p; n = o.n; s = o.s; borrowed = o.borrowed;
+      o.p = nullptr; o.n = 0; o.borrowed = false;
     }
     return *this;
   }
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && !borrowed) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    borrowed = false;
+  }
+  void borrow(T* ptr, i64 count) {
+    release();
+    p = ptr;
+    n = count;
+    borrowed = true;
   }
   void alloc(i64 count, cudaStream_t stream) {
     // free on the caller's (live) stream: a shared scratch may outlive the stream
     // it was first allocated on
-    if (p) cudaFreeAsync(p, stream);
+    if (p && !borrowed) cudaFreeAsync(p, stream);
     p = nullptr;
     n = 0;
+    borrowed = false;
     s = stream;
     n = count;
     if (count > 0) CUDA_CHECK(cudaMallocAsync(&p, sizeof(T) * (size_t)count, stream));

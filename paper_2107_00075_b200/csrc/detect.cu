@@ -195,9 +195,10 @@ __global__ void k_mark_flags(const i32* rows, i64 n, const uint8_t* mark, uint8_
 // ---- free-running D1: pair-centric detection around changed vertices --------
 // Without the reference's ordered replay (every conflicting pair loses its loser),
 // only pairs touching a vertex whose colour changed since the previous detection
-// can conflict.  Each such vertex scans its row; a pair with a ghost end and equal
-// non-zero colours uncolours its loser (degree / gid-hash cascade).  The count is
-// the number of vertices uncoloured (atomicExch makes repeats idempotent).
+// can conflict.  Each such vertex scans its row; a cut pair (one owned, one ghost
+// end) with equal non-zero colours uncolours its loser (degree / gid-hash cascade)
+// on the loser's owner.  The count is the number of vertices uncoloured
+// (atomicExch makes repeats idempotent).
 constexpr i64 DET_HEAVY = 2048;
 constexpr int DET_HEAVY_THREADS = 512;
 
@@ -235,14 +236,57 @@ struct FreeDet {
   const i64* gids;
   const i32* deg;
   bool rd;
+  i32* next = nullptr;                   // optional: owned losers -> next worklist
+  unsigned long long* nnext = nullptr;
+  bool owner_only = true;
 };
 
+// owner_only (worklist-driven path): only the loser's owner uncolours it (owned
+// losers go to the next worklist); ghost copies are written by their owners alone
+// (exchange, and the loser broadcast after detection), so both owners of a cut edge
+// see the same pair and no copy goes stale.  Otherwise (the full exchange rewrites
+// every ghost each round) a ghost loser's copy is zeroed here as well.
 __device__ __forceinline__ int free_pair(const FreeDet& a, i32 x, bool ox, i32 cx, i32 y) {
-  if (ox && a.owned[y]) return 0;
+  const bool oy = a.owned[y];
+  if (ox && oy) return 0;  // owned-owned pairs are proper by construction
+  if (a.owner_only && !ox && !oy) return 0;
   const i32 cy = ld_relaxed(a.colors + y);
   if (cy != cx) return 0;
   const i32 loser = v_loses(a.gids[x], a.gids[y], a.deg[x], a.deg[y], a.rd) ? x : y;
-  return atomicExch(a.colors + loser, 0) != 0 ? 1 : 0;
+  const bool lo = loser == x ? ox : oy;
+  if (a.owner_only && !lo) return 0;  // the ghost loses: its owner uncolours it
+  if (atomicExch(a.colors + loser, 0) == 0) return 0;
+  if (a.next && lo) a.next[atomicAdd(a.nnext, 1ull)] = loser;
+  return 1;
+}
+
+// changed-vertex list -> light / heavy rows (warp-aggregated appends)
+__global__ void k_split_list(const i32* list, const unsigned long long* n_dev, const i64* rowptr, const i32* colors,
+                             i32* light, i32* heavy, unsigned long long* cnt) {
+  const int lane = threadIdx.x & 31;
+  const i64 n = (i64)*n_dev;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 b = (blockIdx.x * (i64)blockDim.x + threadIdx.x) & ~31ll; b < n; b += stride) {
+    const i64 i = b + lane;
+    bool ch = false, h = false;
+    i32 x = 0;
+    if (i < n) {
+      x = list[i];
+      ch = colors[x] != 0;
+      if (ch) h = rowptr[x + 1] - rowptr[x] > DET_HEAVY;
+    }
+    const unsigned mh = __ballot_sync(FULL, ch && h), ml = __ballot_sync(FULL, ch && !h);
+    unsigned long long oh = 0, ol = 0;
+    if (lane == 0) {
+      if (ml) ol = atomicAdd(cnt, (unsigned long long)__popc(ml));
+      if (mh) oh = atomicAdd(cnt + 1, (unsigned long long)__popc(mh));
+    }
+    ol = __shfl_sync(FULL, ol, 0);
+    oh = __shfl_sync(FULL, oh, 0);
+    const unsigned below = lanemask_lt();
+    if (ch && h) heavy[oh + __popc(mh & below)] = x;
+    else if (ch) light[ol + __popc(ml & below)] = x;
+  }
 }
 
 __global__ void k_free_light(FreeDet a, const i32* list, const unsigned long long* n_dev,
@@ -255,10 +299,12 @@ __global__ void k_free_light(FreeDet a, const i32* list, const unsigned long lon
   for (i64 i = warp; i < n; i += nwarps) {
     const i32 x = list[i];
     const bool ox = a.owned[x];
+    const i32 cx0 = ld_relaxed(a.colors + x);
+    if (cx0 == 0) continue;
     const i64 rs = a.rowptr[x], re = a.rowptr[x + 1];
     for (i64 e = rs + lane; e < re; e += 32) {
-      const i32 cx = ld_relaxed(a.colors + x);
-      if (cx == 0) break;  // already uncoloured by another pair
+      const i32 cx = ox ? ld_relaxed(a.colors + x) : cx0;
+      if (cx == 0) break;  // an owned scanner already uncoloured by another pair
       mine += free_pair(a, x, ox, cx, a.col[e]);
     }
   }
@@ -275,9 +321,11 @@ __global__ void __launch_bounds__(DET_HEAVY_THREADS) k_free_heavy(FreeDet a, con
   for (i64 i = blockIdx.x; i < n; i += gridDim.x) {
     const i32 x = list[i];
     const bool ox = a.owned[x];
+    const i32 cx0 = ld_relaxed(a.colors + x);
+    if (cx0 == 0) continue;
     const i64 rs = a.rowptr[x], re = a.rowptr[x + 1];
     for (i64 e = rs + threadIdx.x; e < re; e += DET_HEAVY_THREADS) {
-      const i32 cx = ld_relaxed(a.colors + x);
+      const i32 cx = ox ? ld_relaxed(a.colors + x) : cx0;
       if (cx == 0) break;
       mine += free_pair(a, x, ox, cx, a.col[e]);
     }
@@ -296,7 +344,7 @@ static void run_detect_free_d1(const DetectArgs& A, i64 nv, DetectScratch& S, un
   CUDA_CHECK(cudaMemsetAsync(S.nch.p, 0, 2 * sizeof(unsigned long long), s));
   k_changed_split<<<grid_for(nv, 256, num_sms() * 8), 256, 0, s>>>(
       A.colors, S.prev_valid ? S.prev.p : nullptr, nv, A.rowptr, S.chl.p, S.chh.p, S.nch.p);
-  FreeDet a{A.rowptr, A.col, A.colors, A.owned_flag, A.gids, A.deg, A.recolor_degrees};
+  FreeDet a{A.rowptr, A.col, A.colors, A.owned_flag, A.gids, A.deg, A.recolor_degrees, nullptr, nullptr, false};
   k_free_heavy<<<num_sms() * 4, DET_HEAVY_THREADS, 0, s>>>(a, S.chh.p, S.nch.p + 1, conflicts);
   k_free_light<<<grid_for(nv * 32, 256, num_sms() * 16), 256, 0, s>>>(a, S.chl.p, S.nch.p, conflicts);
   count_launch(3);
@@ -304,6 +352,29 @@ static void run_detect_free_d1(const DetectArgs& A, i64 nv, DetectScratch& S, un
   S.prev.reserve(nv, s);
   CUDA_CHECK(cudaMemcpyAsync(S.prev.p, A.colors, sizeof(i32) * nv, cudaMemcpyDeviceToDevice, s));
   S.prev_valid = true;
+}
+
+void run_detect_free_lists(const DetectArgs& A, i64 nv, const FreeList* lists, int nlists, i32* next,
+                           unsigned long long* nnext, DetectScratch& S, unsigned long long* conflicts,
+                           cudaStream_t s) {
+  i64 cap = 0;
+  for (int i = 0; i < nlists; i++) cap += lists[i].cap;
+  S.chl.reserve(std::max<i64>(cap, 1), s);
+  S.chh.reserve(std::max<i64>(cap, 1), s);
+  S.nch.reserve(2, s);
+  CUDA_CHECK(cudaMemsetAsync(S.nch.p, 0, 2 * sizeof(unsigned long long), s));
+  for (int i = 0; i < nlists; i++) {
+    if (lists[i].cap <= 0) continue;
+    k_split_list<<<grid_for(lists[i].cap, 256, num_sms() * 8), 256, 0, s>>>(
+        lists[i].ids, lists[i].n_dev, A.rowptr, A.colors, S.chl.p, S.chh.p, S.nch.p);
+    count_launch();
+  }
+  FreeDet a{A.rowptr, A.col, A.colors, A.owned_flag, A.gids, A.deg, A.recolor_degrees, next, nnext, true};
+  k_free_heavy<<<num_sms() * 4, DET_HEAVY_THREADS, 0, s>>>(a, S.chh.p, S.nch.p + 1, conflicts);
+  k_free_light<<<grid_for(std::max<i64>(cap, 1) * 32, 256, num_sms() * 16), 256, 0, s>>>(a, S.chl.p, S.nch.p,
+                                                                                        conflicts);
+  count_launch(2);
+  CUDA_CHECK(cudaGetLastError());
 }
 
 void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,

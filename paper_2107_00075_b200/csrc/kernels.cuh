@@ -72,6 +72,8 @@ void launch_scatter_idx_values(i32* dst, const i32* idx, const i32* values, cons
 void launch_clamp_nonneg(i32* dst, const i32* src, i64 n, cudaStream_t s);
 // ordered compaction of indices i in [0,n) with flag[i] != 0; count -> *n_out (device)
 void select_flagged(const uint8_t* flags, i64 n, i32* out, i64* n_out, cudaStream_t s);
+// same, emitting base + i
+void select_flagged_base(const uint8_t* flags, i64 n, i32 base, i32* out, i64* n_out, cudaStream_t s);
 void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* out, i64* n_out,
                            cudaStream_t s);
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s);
@@ -110,6 +112,17 @@ struct DetectScratch {
   DBuf<unsigned long long> nch;
   bool prev_valid = false;
 };
+// Free-running D1 detection around explicit changed-vertex lists (device counts):
+// pairs with a ghost end and equal non-zero colours uncolour their loser; owned
+// losers are appended to next[*nnext].  Adds the number uncoloured to *conflicts.
+struct FreeList {
+  const i32* ids;
+  const unsigned long long* n_dev;
+  i64 cap;
+};
+void run_detect_free_lists(const DetectArgs& A, i64 nv, const FreeList* lists, int nlists, i32* next,
+                           unsigned long long* nnext, DetectScratch& S, unsigned long long* conflicts,
+                           cudaStream_t s);
 // Adds the number of conflicts to *conflicts_dev (device, unsigned long long).
 void run_detect(const DetectArgs& a, i64 num_vertices, DetectScratch& S,
                 unsigned long long* conflicts_dev, cudaStream_t s);

@@ -309,14 +309,27 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   const bool d2 = mode >= CHROMA_MODE_D2;
   const bool partial = mode == CHROMA_MODE_PD2;
   const int dist = d2 ? 2 : 1;
-  const bool gs = algo == CHROMA_ALGO_GAUSS_SEIDEL;
   world_reset_exchange(w);
   w.colors.zero(s);
   w.cs.wl.reserve(w.NL + 1, s);
   w.cs.nwl.reserve(1, s);
   w.cs.flags.reserve(w.NL + 1, s);
-  const i64 nstats = 3 + w.P;
-  std::vector<unsigned long long> hs((size_t)nstats);
+  const i64 nstats = 3 + w.P;  // allreduced; hs[nstats] is this process's next-worklist size
+  std::vector<unsigned long long> hs((size_t)nstats + 1);
+  // Free-running distance-1 fast path: after round 0 the worklist is the owned
+  // losers the detection appended, the exchange walks only that worklist (NVLink
+  // peer stores between processes), and the detection only the pairs around
+  // vertices that changed (worklist + changed ghost copies).
+  static const bool no_fast = std::getenv("CHROMA_NO_FAST_FREE") != nullptr;
+  const bool fast = algo == CHROMA_ALGO_FREE && dist == 1 && !no_fast && (!w.connected || w.p2p || w.P == 1);
+  if (fast) {
+    halo_route_index(w);
+    w.next_wl.reserve(w.NL + 1, s);
+    w.nghost_dev.reserve(1, s);
+    const unsigned long long ng = (unsigned long long)w.NGHOST;
+    CUDA_CHECK(cudaMemcpyAsync(w.nghost_dev.p, &ng, sizeof(ng), cudaMemcpyHostToDevice, s));
+  }
+  i64 nwl_host = w.NL;
   cudaEvent_t ev[8];
   for (auto& e : ev) CUDA_CHECK(cudaEventCreate(&e));
   w.t_total = w.t_color_kernel = w.t_color = w.t_comm = w.t_detect = 0;
@@ -348,35 +361,70 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
       status = CHROMA_ERUNTIME;
       break;
     }
-    CUDA_CHECK(cudaMemsetAsync(w.stats.p, 0, sizeof(unsigned long long) * nstats, s));
+    CUDA_CHECK(cudaMemsetAsync(w.stats.p, 0, sizeof(unsigned long long) * (nstats + 1), s));
     CUDA_CHECK(cudaEventRecord(ev[0], s));
-    // worklist (ordered compaction: ascending local id)
-    // Jacobi re-colours uncoloured ghosts too (F7); the other modes only owned ones
-    k_flag_worklist<<<G(w.NL), 256, 0, s>>>(w.colors.p, w.owned_flag.p, w.NL,
-                                            round == 0 || algo != CHROMA_ALGO_JACOBI, w.cs.flags.p);
-    count_launch();
-    select_flagged(w.cs.flags.p, w.NL, w.cs.wl.p, w.cs.nwl.p, s);
+    if (fast && round > 0) {
+      // the previous detection's owned losers, ascending (the ordered kernel needs it)
+      nwl_host = (i64)hs[(size_t)nstats];
+      sort_i32(w.next_wl.p, nwl_host, s);
+      CUDA_CHECK(cudaMemcpyAsync(w.cs.wl.p, w.next_wl.p, sizeof(i32) * std::max<i64>(nwl_host, 1),
+                                 cudaMemcpyDeviceToDevice, s));
+      CUDA_CHECK(cudaMemcpyAsync(w.cs.nwl.p, &hs[(size_t)nstats], sizeof(i64), cudaMemcpyHostToDevice, s));
+    } else {
+      // worklist (ordered compaction: ascending local id)
+      // Jacobi re-colours uncoloured ghosts too (F7); the other modes only owned ones
+      k_flag_worklist<<<G(w.NL), 256, 0, s>>>(w.colors.p, w.owned_flag.p, w.NL,
+                                              round == 0 || algo != CHROMA_ALGO_JACOBI, w.cs.flags.p);
+      count_launch();
+      select_flagged(w.cs.flags.p, w.NL, w.cs.wl.p, w.cs.nwl.p, s);
+      nwl_host = w.NL;
+    }
     k_count_recolored<<<G(w.NL), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
                                               w.rank_hi - w.rank_lo, w.stats.p);
     count_launch();
     const bool gs_like = algo != CHROMA_ALGO_JACOBI;
-    color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, w.NL, true, dist, partial,
+    color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, nwl_host, true, dist, partial,
               algo, true, w.cs, s, gs_like ? ev[6] : nullptr, gs_like ? ev[7] : nullptr);
     CUDA_CHECK(cudaEventRecord(ev[1], s));
     // exchange: every ghost takes its owner's colour; accounting is changed-only
+    const bool listed = fast && round > 0;  // exchange and detection driven by lists
     if (w.nrouted) {
-      world_exchange_local(w, round > 0, true);
+      if (listed) halo_exchange_local_list(w, w.cs.wl.p, w.cs.nwl.p, nwl_host);
+      else world_exchange_local(w, round > 0, true);
       launch_pair_stats(w.pair_cnt.p, (i64)w.P * w.P, w.stats.p + 1, s);
     }
-    if (remote) exchange_remote(w, round > 0);
+    if (remote) {
+      if (listed) {
+        halo_exchange_p2p(w, w.cs.wl.p, w.cs.nwl.p, nwl_host);
+        launch_pair_stats(w.pair_cnt.p, w.P, w.stats.p + 1, s);
+      } else {
+        exchange_remote(w, round > 0);
+        if (fast) halo_init_p2p_last(w);
+      }
+    }
     CUDA_CHECK(cudaEventRecord(ev[2], s));
-    run_detect(da, w.NL, w.det, w.stats.p, s);
+    if (fast && w.NGHOST == 0) {
+      // no cut edges: a locally proper colouring is final
+    } else if (fast) {
+      FreeList lists[2];
+      lists[0] = {w.cs.wl.p, reinterpret_cast<const unsigned long long*>(w.cs.nwl.p), nwl_host};
+      if (!listed) {
+        lists[1] = {w.ghosts.p, w.nghost_dev.p, w.NGHOST};
+      } else {
+        halo_changed_ghosts(w);  // flags raised by this round's exchange
+        lists[1] = {w.glist.p, w.gcnt.p, w.NGHOST};
+      }
+      run_detect_free_lists(da, w.NL, lists, 2, w.next_wl.p, w.stats.p + nstats, w.det, w.stats.p, s);
+      halo_broadcast_losers(w, w.next_wl.p, w.stats.p + nstats, w.NL);
+    } else {
+      run_detect(da, w.NL, w.det, w.stats.p, s);
+    }
 #ifdef CHROMA_WITH_NCCL
     if (remote)
       NCCL_CHECK(ncclAllReduce(w.stats.p, w.stats.p, nstats, ncclUint64, ncclSum, w.comm, s));
 #endif
     CUDA_CHECK(cudaEventRecord(ev[3], s));
-    CUDA_CHECK(cudaMemcpyAsync(hs.data(), w.stats.p, sizeof(unsigned long long) * nstats,
+    CUDA_CHECK(cudaMemcpyAsync(hs.data(), w.stats.p, sizeof(unsigned long long) * (nstats + 1),
                                cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
     float t01 = 0, t12 = 0, t23 = 0, tk = 0;
@@ -494,6 +542,8 @@ void world_connect(World& w, void* comm, i32 nranks, i32 rank, const i64* send_c
   w.connected = true;
   world_reset_exchange(w);
   CUDA_CHECK(cudaStreamSynchronize(s));
+  halo_release_p2p(w);
+  halo_setup_p2p(w, sl, sp, rl);
 }
 #endif
 

@@ -125,6 +125,19 @@ void select_flagged(const uint8_t* flags, i64 n, i32* out, i64* n_out, cudaStrea
   count_launch();
 }
 
+void select_flagged_base(const uint8_t* flags, i64 n, i32 base, i32* out, i64* n_out, cudaStream_t s) {
+  if (n <= 0) {
+    CUDA_CHECK(cudaMemsetAsync(n_out, 0, sizeof(i64), s));
+    return;
+  }
+  thrust::counting_iterator<i32> it(base);
+  size_t bytes = 0;
+  CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, n_out, n, s));
+  t_cub_tmp.reserve((i64)bytes, s);
+  CUDA_CHECK(cub::DeviceSelect::Flagged(t_cub_tmp.p, bytes, it, flags, out, n_out, n, s));
+  count_launch();
+}
+
 void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* out, i64* n_out,
                            cudaStream_t s) {
   if (n <= 0) {

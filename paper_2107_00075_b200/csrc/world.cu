@@ -549,7 +549,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       w->pair_cnt.zero(s);
     }
     ptm.mark("routing");
-    w->stats.alloc(3 + P, s);
+    w->stats.alloc(4 + P, s);  // [0] conflicts [1] bytes [2] msgs [3..3+P) recolored, [3+P] next worklist
     w->changed.alloc(NL + 1, s);
     world_reset_exchange(*w);
     CUDA_CHECK(cudaStreamSynchronize(s));
@@ -566,6 +566,7 @@ void world_destroy(World* w) {
   cudaSetDevice(w->device);
   cudaStream_t s = w->stream;
   if (s) cudaStreamSynchronize(s);
+  halo_release_p2p(*w);
   delete w;  // the NCCL communicator is borrowed (chroma_comm), not owned
   if (s) cudaStreamDestroy(s);
 }

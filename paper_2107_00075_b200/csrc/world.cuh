@@ -71,6 +71,29 @@ struct World {
 #ifdef CHROMA_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
+  // NVLink peer-memory halo (connected worlds, free-running fast path): this
+  // rank's colours live in an IPC-shared cudaMalloc region [ctrl | colours | flags];
+  // owners store changed colours straight into their peers' ghost slots and raise
+  // the slot's changed flag there.
+  bool p2p = false;
+  void* ipc_base = nullptr;                 // own region (cudaMalloc)
+  std::vector<void*> peer_base;             // opened peer regions (nullptr for self)
+  unsigned long long* my_ctrl = nullptr;    // [1] barrier arrivals
+  uint8_t* my_flag = nullptr;               // changed flag per lid (written by peers)
+  DBuf<i32*> peer_colors;                   // device arrays [P]
+  DBuf<uint8_t*> peer_flag;
+  DBuf<unsigned long long*> peer_ctrl;
+  DBuf<i64> rs_off;                         // owned lid -> send entries (CSR)
+  DBuf<i32> rs_peer, rs_rlid, rs_last;      // per send entry: peer, remote lid, last sent
+  unsigned long long bar_epoch = 0;
+  std::vector<unsigned long long> route_pair_static;  // routes per (src,dst) pair
+  // virtual worlds: owned lid -> routed index (-1: not routed), built lazily
+  DBuf<i32> route_idx;
+  DBuf<i32> glist;                          // changed ghost lids of this round
+  DBuf<unsigned long long> gcnt;
+  DBuf<uint8_t> gflag;                      // changed flag per lid (virtual worlds)
+  DBuf<i32> next_wl;                        // owned losers of the last detection
+  DBuf<unsigned long long> nghost_dev;      // NGHOST on the device (round-0 changed list)
   // protocol scratch
   ColorScratch cs;
   DetectScratch det;
@@ -91,6 +114,18 @@ World* world_create(i64 n, const i64* off, const i64* col, i32 P, const i32* own
 void world_destroy(World* w);
 void world_reset_exchange(World& w);
 void world_exchange_local(World& w, bool changed_only, bool write_all);
+
+// halo_p2p.cu: worklist-driven exchange (free-running distance-1 path)
+void halo_route_index(World& w);
+void halo_exchange_local_list(World& w, const i32* wl, const i64* nwl_dev, i64 nwl_max);
+void halo_exchange_p2p(World& w, const i32* wl, const i64* nwl_dev, i64 nwl_max);
+void halo_init_p2p_last(World& w);
+void halo_changed_ghosts(World& w);  // -> w.glist / w.gcnt (ascending), flags cleared
+// detection's owned losers -> 0 in every ghost copy (owners are the only writers)
+void halo_broadcast_losers(World& w, const i32* list, const unsigned long long* n_dev, i64 n_max);
+void halo_setup_p2p(World& w, const std::vector<i32>& send_lids_abs, const std::vector<i32>& send_peer,
+                    const std::vector<i32>& recv_lids_abs);
+void halo_release_p2p(World& w);
 
 // Colour the worklist of a CSR (absolute vertex ids).  `wl_sorted_unique` skips the
 // device sort/dedupe for protocol worklists that are produced in order.

@@ -38,3 +38,21 @@ def test_dist_parity_nccl(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "mismatches (all ranks) = 0" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("n,p2p", [(2, True), (4, True), (2, False)])
+def test_dist_free_running(n, p2p):
+    """Free-running mode across processes: NVLink peer-memory halo (or NCCL only)."""
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    env = dict(os.environ)
+    if not p2p:
+        env["CHROMA_NO_P2P"] = "1"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "dist_free_main.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert "failures = 0" in r.stdout
