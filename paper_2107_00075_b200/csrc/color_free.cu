@@ -103,30 +103,33 @@ __device__ __forceinline__ int pick(const u32* mw, int& skip) {
   return 0;
 }
 
-template <int DIST, bool PARTIAL>
+// G lanes per vertex (G = 8 for short rows: four vertices in flight per warp; 32 for
+// the rest).  Groups of a warp are independent: reductions use the group's lane mask.
+template <int DIST, bool PARTIAL, int G>
 __global__ void k_color_light(const i64* rowptr, const i32* col, i32* colors, const i32* list, const i64* n_dev,
                               bool snapshot, int rank_cap) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, t = lane % G;
+  const unsigned gmask = G == 32 ? FULL : ((1u << G) - 1) << (lane / G * G);
   const i64 n = *n_dev;
-  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
-  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  for (i64 i = warp; i < n; i += nwarps) {
+  const i64 grp = ((blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5) * (32 / G) + lane / G;
+  const i64 ngrp = (((i64)gridDim.x * blockDim.x) >> 5) * (32 / G);
+  for (i64 i = grp; i < n; i += ngrp) {
     const i32 v = list[i];
     int skip = -1;
     for (i32 base = 1;; base += WIN) {
       Acc a;
       a.clear();
       const bool count = skip < 0;
-      for_each_in_set<DIST, PARTIAL>(rowptr, col, v, lane, 32, [&](i32 x) {
+      for_each_in_set<DIST, PARTIAL>(rowptr, col, v, t, G, [&](i32 x) {
         a.add(x, v, ld_relaxed(colors + x), base, snapshot && count);
       });
-      if (count) skip = snapshot ? min(__reduce_add_sync(FULL, a.rank), rank_cap) : 0;
+      if (count) skip = snapshot ? min((int)__reduce_add_sync(gmask, (unsigned)a.rank), rank_cap) : 0;
       u32 mw[WORDS];
 #pragma unroll
-      for (int w = 0; w < WORDS; w++) mw[w] = __reduce_or_sync(FULL, a.m[w]);
+      for (int w = 0; w < WORDS; w++) mw[w] = __reduce_or_sync(gmask, a.m[w]);
       const int r = pick(mw, skip);
       if (r) {
-        if (lane == 0) st_relaxed(colors + v, -(base + r - 1));
+        if (t == 0) st_relaxed(colors + v, -(base + r - 1));
         break;
       }
     }
@@ -185,33 +188,26 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_color_heavy(const i64* rowptr
 }
 
 // Resolution: v keeps its colour unless a larger-id member of its set has it.
-// Light: each warp takes 32 consecutive list entries, one atomic per group.
-template <int DIST, bool PARTIAL>
+// G lanes per vertex as above; losers are a small fraction, one atomic each.
+template <int DIST, bool PARTIAL, int G>
 __global__ void k_losers_light(const i64* rowptr, const i32* col, i32* colors, const i32* list, const i64* n_dev,
                                i32* next, unsigned long long* nnext) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, t = lane % G;
+  const unsigned gmask = G == 32 ? FULL : ((1u << G) - 1) << (lane / G * G);
   const i64 n = *n_dev;
-  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
-  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  for (i64 g = warp * 32; g < n; g += nwarps * 32) {
-    const int cnt = n - g < 32 ? (int)(n - g) : 32;
-    u32 lose = 0;
-    for (int j = 0; j < cnt; j++) {
-      const i32 v = list[g + j];
-      const i32 c = iabs(ld_relaxed(colors + v));
-      bool hit = false;
-      for_each_in_set<DIST, PARTIAL>(rowptr, col, v, lane, 32, [&](i32 x) {
-        if (x > v && iabs(ld_relaxed(colors + x)) == c) hit = true;
-      });
-      const bool any = __any_sync(FULL, hit);
-      if (lane == 0) st_relaxed(colors + v, any ? 0 : c);
-      if (any) lose |= 1u << j;
-    }
-    if (lose) {
-      unsigned long long off = 0;
-      if (lane == 0) off = atomicAdd(nnext, (unsigned long long)__popc(lose));
-      off = __shfl_sync(FULL, off, 0);
-      if (lose >> lane & 1) next[off + __popc(lose & ((1u << lane) - 1))] = list[g + lane];
+  const i64 grp = ((blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5) * (32 / G) + lane / G;
+  const i64 ngrp = (((i64)gridDim.x * blockDim.x) >> 5) * (32 / G);
+  for (i64 i = grp; i < n; i += ngrp) {
+    const i32 v = list[i];
+    const i32 c = iabs(ld_relaxed(colors + v));
+    bool hit = false;
+    for_each_in_set<DIST, PARTIAL>(rowptr, col, v, t, G, [&](i32 x) {
+      if (x > v && iabs(ld_relaxed(colors + x)) == c) hit = true;
+    });
+    const bool any = __any_sync(gmask, hit);
+    if (t == 0) {
+      st_relaxed(colors + v, any ? 0 : c);
+      if (any) next[atomicAdd(nnext, 1ull)] = v;
     }
   }
 }
@@ -242,9 +238,9 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_losers_heavy(const i64* rowpt
   }
 }
 
-// worklist -> light / heavy lists (warp-aggregated appends)
-__global__ void k_split(const i32* wl, const i64* n_dev, const i64* rowptr, i64 heavy_deg, i32* light,
-                        unsigned long long* nlight, i32* heavy, unsigned long long* nheavy) {
+// worklist -> tiny / light / heavy lists by row length (warp-aggregated appends)
+__global__ void k_split(const i32* wl, const i64* n_dev, const i64* rowptr, i64 tiny_deg, i64 heavy_deg, i32* tiny,
+                        i32* light, i32* heavy, unsigned long long* cnt /* [light, heavy, tiny] */) {
   const int lane = threadIdx.x & 31;
   const i64 n = *n_dev;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -252,18 +248,18 @@ __global__ void k_split(const i32* wl, const i64* n_dev, const i64* rowptr, i64 
     const i64 i = b + lane;
     const bool valid = i < n;
     const i32 v = valid ? wl[i] : 0;
-    const bool h = valid && rowptr[v + 1] - rowptr[v] > heavy_deg;
-    const u32 mh = __ballot_sync(FULL, h), ml = __ballot_sync(FULL, valid && !h);
-    unsigned long long oh = 0, ol = 0;
-    if (lane == 0) {
-      if (mh) oh = atomicAdd(nheavy, (unsigned long long)__popc(mh));
-      if (ml) ol = atomicAdd(nlight, (unsigned long long)__popc(ml));
-    }
-    oh = __shfl_sync(FULL, oh, 0);
-    ol = __shfl_sync(FULL, ol, 0);
+    const i64 d = valid ? rowptr[v + 1] - rowptr[v] : 0;
+    const int cls = !valid ? -1 : d > heavy_deg ? 1 : d <= tiny_deg ? 2 : 0;
     const u32 below = (1u << lane) - 1;
-    if (h) heavy[oh + __popc(mh & below)] = v;
-    else if (valid) light[ol + __popc(ml & below)] = v;
+    i32* out[3] = {light, heavy, tiny};
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const u32 m = __ballot_sync(FULL, cls == k);
+      unsigned long long o = 0;
+      if (lane == 0 && m) o = atomicAdd(cnt + k, (unsigned long long)__popc(m));
+      o = __shfl_sync(FULL, o, 0);
+      if (cls == k) out[k][o + __popc(m & below)] = v;
+    }
   }
 }
 
@@ -486,40 +482,52 @@ __global__ void k_unkey(const u64* keys, i64 n, i32* v) {
     CUDA_CHECK(cudaGetLastError());                                                         \
   } while (0)
 
+#define FREE_DISPATCH_G(KERNEL, G, GRID, BLOCK, ...)                                        \
+  do {                                                                                      \
+    if (dist == 1) KERNEL<1, false, G><<<GRID, BLOCK, 0, s>>>(__VA_ARGS__);                 \
+    else if (partial) KERNEL<2, true, G><<<GRID, BLOCK, 0, s>>>(__VA_ARGS__);               \
+    else KERNEL<2, false, G><<<GRID, BLOCK, 0, s>>>(__VA_ARGS__);                           \
+    count_launch();                                                                         \
+    CUDA_CHECK(cudaGetLastError());                                                         \
+  } while (0)
+
 }  // namespace
 
-void launch_free_split(const i32* wl, const i64* n_dev, i64 n_max, const i64* rowptr, i64 heavy_deg, FreeLists& f,
-                       int p, cudaStream_t s) {
-  CUDA_CHECK(cudaMemsetAsync(f.cnt + 2 * p, 0, 2 * sizeof(i64), s));
+void launch_free_split(const i32* wl, const i64* n_dev, i64 n_max, const i64* rowptr, i64 tiny_deg, i64 heavy_deg,
+                       FreeLists& f, int p, cudaStream_t s) {
+  CUDA_CHECK(cudaMemsetAsync(f.cnt + 3 * p, 0, 3 * sizeof(i64), s));
   if (n_max <= 0) return;
   k_split<<<grid_for(n_max, 256, num_sms() * 8), 256, 0, s>>>(
-      wl, n_dev, rowptr, heavy_deg, f.light[p], reinterpret_cast<unsigned long long*>(f.cnt + 2 * p), f.heavy[p],
-      reinterpret_cast<unsigned long long*>(f.cnt + 2 * p + 1));
+      wl, n_dev, rowptr, tiny_deg, heavy_deg, f.tiny[p], f.light[p], f.heavy[p],
+      reinterpret_cast<unsigned long long*>(f.cnt + 3 * p));
   count_launch();
   CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_free_iteration(const i64* rowptr, const i32* col, i32* colors, FreeLists& f, int p, i64 nlight_max,
-                           i64 nheavy_max, int rank_cap, int dist, bool partial, cudaStream_t s) {
+void launch_free_iteration(const i64* rowptr, const i32* col, i32* colors, FreeLists& f, int p, const i64* nmax,
+                           int rank_cap, int dist, bool partial, cudaStream_t s) {
   const bool snapshot = rank_cap > 0;
   const int q = p ^ 1;
-  CUDA_CHECK(cudaMemsetAsync(f.cnt + 2 * q, 0, 2 * sizeof(i64), s));
-  const int gl = grid_for(std::max<i64>(nlight_max, 1) * 32, 256, num_sms() * 16);
+  const i64 nlight_max = nmax[0], nheavy_max = nmax[1], ntiny_max = nmax[2];
+  CUDA_CHECK(cudaMemsetAsync(f.cnt + 3 * q, 0, 3 * sizeof(i64), s));
+  auto* next_cnt = reinterpret_cast<unsigned long long*>(f.cnt + 3 * q);
+  const i64* cnt = f.cnt + 3 * p;
   const int gh = (int)std::max<i64>(1, std::min<i64>(nheavy_max, num_sms() * 4));
-  auto* nl_next = reinterpret_cast<unsigned long long*>(f.cnt + 2 * q);
-  auto* nh_next = reinterpret_cast<unsigned long long*>(f.cnt + 2 * q + 1);
+  const int gl = grid_for(std::max<i64>(nlight_max, 1) * 32, 256, num_sms() * 16);
+  const int gt = grid_for(std::max<i64>(ntiny_max, 1) * 8, 256, num_sms() * 16);
   if (nheavy_max > 0)
-    FREE_DISPATCH(k_color_heavy, gh, HEAVY_THREADS, rowptr, col, colors, f.heavy[p], f.cnt + 2 * p + 1, snapshot,
-                  rank_cap);
+    FREE_DISPATCH(k_color_heavy, gh, HEAVY_THREADS, rowptr, col, colors, f.heavy[p], cnt + 1, snapshot, rank_cap);
   if (nlight_max > 0)
-    FREE_DISPATCH(k_color_light, gl, 256, rowptr, col, colors, f.light[p], f.cnt + 2 * p, snapshot, rank_cap);
+    FREE_DISPATCH_G(k_color_light, 32, gl, 256, rowptr, col, colors, f.light[p], cnt + 0, snapshot, rank_cap);
+  if (ntiny_max > 0)
+    FREE_DISPATCH_G(k_color_light, 8, gt, 256, rowptr, col, colors, f.tiny[p], cnt + 2, snapshot, rank_cap);
   if (nheavy_max > 0)
-    FREE_DISPATCH(k_losers_heavy, gh, HEAVY_THREADS, rowptr, col, colors, f.heavy[p], f.cnt + 2 * p + 1,
-                  f.heavy[q], nh_next);
-  if (nlight_max > 0) {
-    const int gg = grid_for(std::max<i64>(nlight_max, 1), 256, num_sms() * 16);
-    FREE_DISPATCH(k_losers_light, gg, 256, rowptr, col, colors, f.light[p], f.cnt + 2 * p, f.light[q], nl_next);
-  }
+    FREE_DISPATCH(k_losers_heavy, gh, HEAVY_THREADS, rowptr, col, colors, f.heavy[p], cnt + 1, f.heavy[q],
+                  next_cnt + 1);
+  if (nlight_max > 0)
+    FREE_DISPATCH_G(k_losers_light, 32, gl, 256, rowptr, col, colors, f.light[p], cnt + 0, f.light[q], next_cnt + 0);
+  if (ntiny_max > 0)
+    FREE_DISPATCH_G(k_losers_light, 8, gt, 256, rowptr, col, colors, f.tiny[p], cnt + 2, f.tiny[q], next_cnt + 2);
 }
 
 }  // namespace chroma

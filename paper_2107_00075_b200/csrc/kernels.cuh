@@ -36,13 +36,22 @@ void launch_jacobi_losers(const i64* rowptr, const i32* col, i32* colors, const 
                           uint8_t* lose, int dist, bool partial, cudaStream_t s);
 
 // Free-running speculative colouring (deterministic=False, algorithm="free").
-// Pending vertices are kept in light (warp per vertex) and heavy (CTA per vertex)
-// lists, double-buffered by parity p; cnt[2p] / cnt[2p+1] are their lengths.
+// Pending vertices are kept in light (warp per vertex), heavy (CTA per vertex) and
+// tiny (8 lanes per vertex) lists, double-buffered by parity p; cnt[3p + {0,1,2}]
+// are the light / heavy / tiny lengths.
 struct FreeLists {
   i32* light[2];
   i32* heavy[2];
-  i64* cnt;  // [4]
+  i32* tiny[2];
+  i64* cnt;  // [6]
 };
+void launch_free_split(const i32* wl, const i64* n_dev, i64 n_max, const i64* rowptr, i64 tiny_deg, i64 heavy_deg,
+                       FreeLists& f, int p, cudaStream_t s);
+// colour lists[p] (rank_cap > 0: snapshot rank-offset first fit, skipping up to
+// rank_cap free colours), resolve, losers -> lists[p^1]; nmax = host upper bounds
+// of the three lengths
+void launch_free_iteration(const i64* rowptr, const i32* col, i32* colors, FreeLists& f, int p, const i64* nmax,
+                           int rank_cap, int dist, bool partial, cudaStream_t s);
 struct FreeWaveScratch {
   DBuf<u32> F, A;
   DBuf<int> ovf;

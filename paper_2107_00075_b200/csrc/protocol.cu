@@ -32,8 +32,9 @@ __global__ void k_flag_worklist(const i32* colors, const uint8_t* owned_flag, i6
     flag[i] = (colors[i] == 0 && (!owned_only || owned_flag[i])) ? 1 : 0;
 }
 
-// recolored_per_rank: owned entries of the worklist per local rank (block-local
-// histogram in shared memory, one global atomic per block and rank)
+// recolored_per_rank: owned entries of the worklist per local rank.  Worklists are
+// ascending, so a thread's entries mostly share one rank: count runs in a register,
+// flush into a block histogram on change, one global atomic per block and rank.
 __global__ void k_count_recolored(const i32* wl, const i64* nwl, const uint8_t* owned_flag,
                                   const i32* rank_of, i32 rank_lo, i32 nlocal, unsigned long long* stats) {
   __shared__ unsigned long long h[256];
@@ -42,13 +43,25 @@ __global__ void k_count_recolored(const i32* wl, const i64* nwl, const uint8_t* 
     for (int i = threadIdx.x; i < nlocal; i += blockDim.x) h[i] = 0;
   __syncthreads();
   const i64 n = *nwl;
+  i32 cur = -1;
+  unsigned long long run = 0;
+  auto flush = [&]() {
+    if (run == 0) return;
+    if (local_hist) atomicAdd(&h[cur], run);
+    else atomicAdd(&stats[3 + rank_lo + cur], run);
+    run = 0;
+  };
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 v = wl[i];
-    if (owned_flag[v]) {
-      if (local_hist) atomicAdd(&h[rank_of[v]], 1ull);
-      else atomicAdd(&stats[3 + rank_lo + rank_of[v]], 1ull);
+    if (!owned_flag[v]) continue;
+    const i32 r = rank_of[v];
+    if (r != cur) {
+      flush();
+      cur = r;
     }
+    run++;
   }
+  flush();
   __syncthreads();
   if (local_hist)
     for (int i = threadIdx.x; i < nlocal; i += blockDim.x)
@@ -115,19 +128,22 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     // dense core to speculate around: it takes the ordered dataflow kernel instead,
     // which is conflict-free and uses the reference's colour count.
     for (auto& b : S.fl) b.reserve(nwl_max, s);
-    S.fcnt.reserve(4, s);
-    FreeLists f{{S.fl[0].p, S.fl[1].p}, {S.fl[2].p, S.fl[3].p}, S.fcnt.p};
-    static const i64 heavy_deg = env_i64("CHROMA_FREE_HEAVY", 1024);
+    S.fcnt.reserve(6, s);
+    FreeLists f{{S.fl[0].p, S.fl[1].p}, {S.fl[2].p, S.fl[3].p}, {S.fl[4].p, S.fl[5].p}, S.fcnt.p};
+    static const i64 heavy_deg = env_i64("CHROMA_FREE_HEAVY", 4096);
     static const i64 rank_cap = env_i64("CHROMA_FREE_RANKCAP", 0);
     static const bool trace = std::getenv("CHROMA_FREE_TRACE") != nullptr;
     static const bool no_waves = std::getenv("CHROMA_FREE_NOWAVES") != nullptr;
     static const bool always_spec = std::getenv("CHROMA_FREE_SPECULATE") != nullptr;
     if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
-    launch_free_split(wl, nwl, nwl_max, rowptr, heavy_deg, f, 0, s);
-    i64 cnt[4];
-    CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 2 * sizeof(i64), cudaMemcpyDeviceToHost, s));
+    static const i64 tiny_deg = env_i64("CHROMA_FREE_TINY", 32);
+    static const i64 tail_n = env_i64("CHROMA_FREE_TAIL", 4096);
+    static const i64 tail_after = env_i64("CHROMA_FREE_TAIL_AFTER", 2);
+    launch_free_split(wl, nwl, nwl_max, rowptr, dist == 1 ? tiny_deg : -1, heavy_deg, f, 0, s);
+    i64 cnt[6];
+    CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 3 * sizeof(i64), cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-    if (dist == 1 && cnt[1] == 0 && !always_spec) {
+    if (dist == 1 && cnt[1] == 0 && !always_spec) {  // no heavy rows
       algo = CHROMA_ALGO_GAUSS_SEIDEL;
       goto gauss_seidel;
     }
@@ -144,7 +160,7 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
       const i64 nh = cnt[1];
       launch_free_heavy(rowptr, col, cur, f.heavy[0], cnt[1], f.light[0], f.cnt, dist, partial, S.fw, s);
       CUDA_CHECK(cudaMemsetAsync(f.cnt + 1, 0, sizeof(i64), s));
-      CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 2 * sizeof(i64), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 3 * sizeof(i64), cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
       if (trace)
         std::fprintf(stderr, "[free] heavy waves (%lld vertices) %.1f us, light %lld\n", (long long)nh,
@@ -153,14 +169,30 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     }
     for (int it = 0; it < MAX_SWEEPS; it++) {
       const int p = it & 1, q = p ^ 1;
-      launch_free_iteration(rowptr, col, cur, f, p, cnt[2 * p], cnt[2 * p + 1], it > 0 ? (int)rank_cap : 0,
-                            dist, partial, s);
-      CUDA_CHECK(cudaMemcpyAsync(cnt + 2 * q, S.fcnt.p + 2 * q, 2 * sizeof(i64), cudaMemcpyDeviceToHost, s));
+      launch_free_iteration(rowptr, col, cur, f, p, cnt + 3 * p, it > 0 ? (int)rank_cap : 0, dist, partial, s);
+      CUDA_CHECK(cudaMemcpyAsync(cnt + 3 * q, S.fcnt.p + 3 * q, 3 * sizeof(i64), cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
       if (trace)
-        std::fprintf(stderr, "[free] it=%d light %lld -> %lld heavy %lld -> %lld\n", it, (long long)cnt[2 * p],
-                     (long long)cnt[2 * q], (long long)cnt[2 * p + 1], (long long)cnt[2 * q + 1]);
-      if (cnt[2 * q] == 0 && cnt[2 * q + 1] == 0) {
+        std::fprintf(stderr, "[free] it=%d light %lld -> %lld heavy %lld -> %lld tiny %lld -> %lld\n", it,
+                     (long long)cnt[3 * p], (long long)cnt[3 * q], (long long)cnt[3 * p + 1],
+                     (long long)cnt[3 * q + 1], (long long)cnt[3 * p + 2], (long long)cnt[3 * q + 2]);
+      const i64 pend = cnt[3 * q] + cnt[3 * q + 1] + cnt[3 * q + 2];
+      if (pend > 0 && it + 1 >= tail_after && pend <= tail_n && !no_waves) {
+        // a small remainder that keeps colliding is a dense cluster: finish it
+        // exactly with the wave kernel instead of iterating one layer at a time
+        i32* dst = f.heavy[q];
+        i64 k = cnt[3 * q + 1];
+        CUDA_CHECK(cudaMemcpyAsync(dst + k, f.light[q], sizeof(i32) * cnt[3 * q], cudaMemcpyDeviceToDevice, s));
+        k += cnt[3 * q];
+        CUDA_CHECK(cudaMemcpyAsync(dst + k, f.tiny[q], sizeof(i32) * cnt[3 * q + 2], cudaMemcpyDeviceToDevice, s));
+        k += cnt[3 * q + 2];
+        CUDA_CHECK(cudaMemsetAsync(f.cnt + 3 * q, 0, 3 * sizeof(i64), s));
+        launch_free_heavy(rowptr, col, cur, dst, k, f.light[q], f.cnt + 3 * q, dist, partial, S.fw, s);
+        CUDA_CHECK(cudaMemcpyAsync(cnt + 3 * q, S.fcnt.p + 3 * q, 3 * sizeof(i64), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (trace) std::fprintf(stderr, "[free] tail waves over %lld, %lld left\n", (long long)k, (long long)cnt[3 * q]);
+      }
+      if (cnt[3 * q] == 0 && cnt[3 * q + 1] == 0 && cnt[3 * q + 2] == 0) {
         if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
         if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
         return;
@@ -406,15 +438,18 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     if (fast && w.NGHOST == 0) {
       // no cut edges: a locally proper colouring is final
     } else if (fast) {
+      // every cut pair sits in a ghost row, so when every vertex changed (round 0)
+      // the ghost rows alone cover the scan; later rounds add the recoloured owned rows
       FreeList lists[2];
-      lists[0] = {w.cs.wl.p, reinterpret_cast<const unsigned long long*>(w.cs.nwl.p), nwl_host};
+      int nl = 0;
       if (!listed) {
-        lists[1] = {w.ghosts.p, w.nghost_dev.p, w.NGHOST};
+        lists[nl++] = {w.ghosts.p, w.nghost_dev.p, w.NGHOST};
       } else {
+        lists[nl++] = {w.cs.wl.p, reinterpret_cast<const unsigned long long*>(w.cs.nwl.p), nwl_host};
         halo_changed_ghosts(w);  // flags raised by this round's exchange
-        lists[1] = {w.glist.p, w.gcnt.p, w.NGHOST};
+        lists[nl++] = {w.glist.p, w.gcnt.p, w.NGHOST};
       }
-      run_detect_free_lists(da, w.NL, lists, 2, w.next_wl.p, w.stats.p + nstats, w.det, w.stats.p, s);
+      run_detect_free_lists(da, w.NL, lists, nl, w.next_wl.p, w.stats.p + nstats, w.det, w.stats.p, s);
       halo_broadcast_losers(w, w.next_wl.p, w.stats.p + nstats, w.NL);
     } else {
       run_detect(da, w.NL, w.det, w.stats.p, s);

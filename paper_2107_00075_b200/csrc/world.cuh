@@ -33,7 +33,7 @@ struct ColorScratch {
   DBuf<i64> nwl, np2;
   DBuf<uint8_t> flags, in_round;
   DBuf<unsigned long long> ticket;
-  DBuf<i32> fl[4];  // free-running light/heavy lists x 2
+  DBuf<i32> fl[6];  // free-running light/heavy/tiny lists x 2
   DBuf<i64> fcnt;
   FreeWaveScratch fw;
 };

@@ -18,7 +18,8 @@ alg = os.environ.get("ALG", "free")
 g = G.gen_rmat(sc, 16, 1, device=f"cuda:{local}")
 pm = PT.partition_block(g, N)
 w = DistWorld(g, pm, 1)
-cfg = R.AlgorithmConfig(mode=R.Mode("d1"), deterministic=alg == "gs", algorithm=None if alg == "gs" else alg)
+cfg = R.AlgorithmConfig(mode=R.Mode("d1"), deterministic=alg == "gs", algorithm=None if alg == "gs" else alg,
+                        recolor_degrees=bool(int(os.environ.get("RD", "0"))))
 out = torch.empty(w.output_length(), dtype=torch.int32, device=f"cuda:{local}")
 for it in range(3):
     dist.barrier()
@@ -26,7 +27,7 @@ for it in range(3):
     _, reps = R.run_distributed(w, cfg, out=out)
     el = time.perf_counter() - t0
 if rank == 0:
-    print(f"N={N} scale={sc} alg={alg} rounds={len(reps)} wall={el*1e3:.1f} ms colors(rank0 max)={int(out.max())}")
+    print(f"N={N} scale={sc} alg={alg} rd={cfg.recolor_degrees} rounds={len(reps)} wall={el*1e3:.1f} ms colors(rank0 max)={int(out.max())}")
     tc = sum(r.time_color_s for r in reps); tm = sum(r.time_comm_s for r in reps); td = sum(r.time_detect_s for r in reps)
     print(f"  sum color={tc*1e3:.2f} comm={tm*1e3:.2f} detect={td*1e3:.2f} ms")
     for r in reps:
