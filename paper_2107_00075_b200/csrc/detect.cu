@@ -236,33 +236,44 @@ struct FreeDet {
   const i64* gids;
   const i32* deg;
   bool rd;
-  i32* next = nullptr;                   // optional: owned losers -> next worklist
-  unsigned long long* nnext = nullptr;
-  bool owner_only = true;
+  bool kill_anywhere = false;            // list path: kill at the loser's owner (KillRoute)
+  KillRoute kr;
 };
 
-// owner_only (worklist-driven path): only the loser's owner uncolours it (owned
-// losers go to the next worklist); ghost copies are written by their owners alone
-// (exchange, and the loser broadcast after detection), so both owners of a cut edge
-// see the same pair and no copy goes stale.  Otherwise (the full exchange rewrites
-// every ghost each round) a ghost loser's copy is zeroed here as well.
+// kill_anywhere (worklist-driven path): the loser is uncoloured at its owner --
+// here if owned, else through KillRoute (same array for virtual ranks, NVLink for
+// peers) -- and its owner's loser flag is raised; ghost copies are then refreshed
+// by their owners alone (loser broadcast, exchange).  Otherwise (the full exchange
+// rewrites every ghost each round) the loser's local entry is zeroed, ghost or not.
 __device__ __forceinline__ int free_pair(const FreeDet& a, i32 x, bool ox, i32 cx, i32 y) {
   const bool oy = a.owned[y];
-  if (ox && oy) return 0;  // owned-owned pairs are proper by construction
-  if (a.owner_only && !ox && !oy) return 0;
+  if (ox == oy) return 0;  // owned-owned is proper by construction; ghost-ghost is the owners' business
   const i32 cy = ld_relaxed(a.colors + y);
   if (cy != cx) return 0;
   const i32 loser = v_loses(a.gids[x], a.gids[y], a.deg[x], a.deg[y], a.rd) ? x : y;
+  if (!a.kill_anywhere) return atomicExch(a.colors + loser, 0) != 0 ? 1 : 0;
   const bool lo = loser == x ? ox : oy;
-  if (a.owner_only && !lo) return 0;  // the ghost loses: its owner uncolours it
-  if (atomicExch(a.colors + loser, 0) == 0) return 0;
-  if (a.next && lo) a.next[atomicAdd(a.nnext, 1ull)] = loser;
+  if (lo) {
+    if (atomicExch(a.colors + loser, 0) == 0) return 0;
+    a.kr.flags[loser] = 1;
+    return 1;
+  }
+  const i32 o = a.kr.owner_lid[loser];
+  const i32 p = a.kr.owner_rank[loser];
+  if (p < 0) {
+    if (atomicExch(a.colors + o, 0) == 0) return 0;
+    a.kr.flags[o] = 1;
+  } else {
+    if (atomicExch_system(a.kr.peer_colors[p] + o, 0) == 0) return 0;
+    a.kr.peer_flag[p][o] = 1;
+  }
   return 1;
 }
 
-// changed-vertex list -> light / heavy rows (warp-aggregated appends)
+// changed-vertex list -> light / heavy rows (warp-aggregated appends; two-hop walks
+// count as heavy from a quarter of the one-hop threshold)
 __global__ void k_split_list(const i32* list, const unsigned long long* n_dev, const i64* rowptr, const i32* colors,
-                             i32* light, i32* heavy, unsigned long long* cnt) {
+                             i64 heavy_deg, i32* light, i32* heavy, unsigned long long* cnt) {
   const int lane = threadIdx.x & 31;
   const i64 n = (i64)*n_dev;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -273,7 +284,7 @@ __global__ void k_split_list(const i32* list, const unsigned long long* n_dev, c
     if (i < n) {
       x = list[i];
       ch = colors[x] != 0;
-      if (ch) h = rowptr[x + 1] - rowptr[x] > DET_HEAVY;
+      if (ch) h = rowptr[x + 1] - rowptr[x] > heavy_deg;
     }
     const unsigned mh = __ballot_sync(FULL, ch && h), ml = __ballot_sync(FULL, ch && !h);
     unsigned long long oh = 0, ol = 0;
@@ -289,6 +300,38 @@ __global__ void k_split_list(const i32* list, const unsigned long long* n_dev, c
   }
 }
 
+// Visit the colouring set of x -- N(x) (D1), N(x) and N2(x) (D2) or N2(x) (PD2) --
+// with `stride` cooperating threads; f returns false to stop this thread's walk.
+template <int DIST, bool PARTIAL, typename F>
+__device__ __forceinline__ void walk_set(const FreeDet& a, i32 x, int t, int stride, F&& f) {
+  const i64 rs = a.rowptr[x], re = a.rowptr[x + 1];
+  if (DIST == 1) {
+    for (i64 e = rs + t; e < re; e += stride)
+      if (!f(a.col[e])) return;
+  } else if (stride == 32) {
+    for (i64 e = rs; e < re; e++) {
+      const i32 u = a.col[e];
+      if (!PARTIAL && t == 0 && !f(u)) return;
+      const i64 ue = a.rowptr[u + 1];
+      for (i64 g = a.rowptr[u] + t; g < ue; g += 32) {
+        const i32 y = a.col[g];
+        if (y != x && !f(y)) return;
+      }
+    }
+  } else {
+    for (i64 e = rs + t; e < re; e += stride) {
+      const i32 u = a.col[e];
+      if (!PARTIAL && !f(u)) return;
+      const i64 ue = a.rowptr[u + 1];
+      for (i64 g = a.rowptr[u]; g < ue; g++) {
+        const i32 y = a.col[g];
+        if (y != x && !f(y)) return;
+      }
+    }
+  }
+}
+
+template <int DIST, bool PARTIAL>
 __global__ void k_free_light(FreeDet a, const i32* list, const unsigned long long* n_dev,
                              unsigned long long* conflicts) {
   const int lane = threadIdx.x & 31;
@@ -301,17 +344,18 @@ __global__ void k_free_light(FreeDet a, const i32* list, const unsigned long lon
     const bool ox = a.owned[x];
     const i32 cx0 = ld_relaxed(a.colors + x);
     if (cx0 == 0) continue;
-    const i64 rs = a.rowptr[x], re = a.rowptr[x + 1];
-    for (i64 e = rs + lane; e < re; e += 32) {
+    walk_set<DIST, PARTIAL>(a, x, lane, 32, [&](i32 y) {
       const i32 cx = ox ? ld_relaxed(a.colors + x) : cx0;
-      if (cx == 0) break;  // an owned scanner already uncoloured by another pair
-      mine += free_pair(a, x, ox, cx, a.col[e]);
-    }
+      if (cx == 0) return false;  // an owned scanner already uncoloured by another pair
+      mine += free_pair(a, x, ox, cx, y);
+      return true;
+    });
   }
   mine = __reduce_add_sync(FULL, mine);
   if (lane == 0 && mine) atomicAdd(conflicts, (unsigned long long)mine);
 }
 
+template <int DIST, bool PARTIAL>
 __global__ void __launch_bounds__(DET_HEAVY_THREADS) k_free_heavy(FreeDet a, const i32* list,
                                                                   const unsigned long long* n_dev,
                                                                   unsigned long long* conflicts) {
@@ -323,16 +367,24 @@ __global__ void __launch_bounds__(DET_HEAVY_THREADS) k_free_heavy(FreeDet a, con
     const bool ox = a.owned[x];
     const i32 cx0 = ld_relaxed(a.colors + x);
     if (cx0 == 0) continue;
-    const i64 rs = a.rowptr[x], re = a.rowptr[x + 1];
-    for (i64 e = rs + threadIdx.x; e < re; e += DET_HEAVY_THREADS) {
+    walk_set<DIST, PARTIAL>(a, x, threadIdx.x, DET_HEAVY_THREADS, [&](i32 y) {
       const i32 cx = ox ? ld_relaxed(a.colors + x) : cx0;
-      if (cx == 0) break;
-      mine += free_pair(a, x, ox, cx, a.col[e]);
-    }
+      if (cx == 0) return false;
+      mine += free_pair(a, x, ox, cx, y);
+      return true;
+    });
   }
   mine = __reduce_add_sync(FULL, mine);
   if (lane == 0 && mine) atomicAdd(conflicts, (unsigned long long)mine);
 }
+
+#define FREE_DET_DISPATCH(KERNEL, GRID, BLOCK, ...)                                          \
+  do {                                                                                      \
+    if (A.dist == 1) KERNEL<1, false><<<GRID, BLOCK, 0, s>>>(__VA_ARGS__);                  \
+    else if (A.partial) KERNEL<2, true><<<GRID, BLOCK, 0, s>>>(__VA_ARGS__);                \
+    else KERNEL<2, false><<<GRID, BLOCK, 0, s>>>(__VA_ARGS__);                              \
+    count_launch();                                                                         \
+  } while (0)
 
 }  // namespace
 
@@ -344,9 +396,9 @@ static void run_detect_free_d1(const DetectArgs& A, i64 nv, DetectScratch& S, un
   CUDA_CHECK(cudaMemsetAsync(S.nch.p, 0, 2 * sizeof(unsigned long long), s));
   k_changed_split<<<grid_for(nv, 256, num_sms() * 8), 256, 0, s>>>(
       A.colors, S.prev_valid ? S.prev.p : nullptr, nv, A.rowptr, S.chl.p, S.chh.p, S.nch.p);
-  FreeDet a{A.rowptr, A.col, A.colors, A.owned_flag, A.gids, A.deg, A.recolor_degrees, nullptr, nullptr, false};
-  k_free_heavy<<<num_sms() * 4, DET_HEAVY_THREADS, 0, s>>>(a, S.chh.p, S.nch.p + 1, conflicts);
-  k_free_light<<<grid_for(nv * 32, 256, num_sms() * 16), 256, 0, s>>>(a, S.chl.p, S.nch.p, conflicts);
+  FreeDet a{A.rowptr, A.col, A.colors, A.owned_flag, A.gids, A.deg, A.recolor_degrees, false, KillRoute{}};
+  k_free_heavy<1, false><<<num_sms() * 4, DET_HEAVY_THREADS, 0, s>>>(a, S.chh.p, S.nch.p + 1, conflicts);
+  k_free_light<1, false><<<grid_for(nv * 32, 256, num_sms() * 16), 256, 0, s>>>(a, S.chl.p, S.nch.p, conflicts);
   count_launch(3);
   CUDA_CHECK(cudaGetLastError());
   S.prev.reserve(nv, s);
@@ -354,9 +406,8 @@ static void run_detect_free_d1(const DetectArgs& A, i64 nv, DetectScratch& S, un
   S.prev_valid = true;
 }
 
-void run_detect_free_lists(const DetectArgs& A, i64 nv, const FreeList* lists, int nlists, i32* next,
-                           unsigned long long* nnext, DetectScratch& S, unsigned long long* conflicts,
-                           cudaStream_t s) {
+void run_detect_free_lists(const DetectArgs& A, i64 nv, const FreeList* lists, int nlists, const KillRoute& kr,
+                           DetectScratch& S, unsigned long long* conflicts, cudaStream_t s) {
   i64 cap = 0;
   for (int i = 0; i < nlists; i++) cap += lists[i].cap;
   S.chl.reserve(std::max<i64>(cap, 1), s);
@@ -366,14 +417,14 @@ void run_detect_free_lists(const DetectArgs& A, i64 nv, const FreeList* lists, i
   for (int i = 0; i < nlists; i++) {
     if (lists[i].cap <= 0) continue;
     k_split_list<<<grid_for(lists[i].cap, 256, num_sms() * 8), 256, 0, s>>>(
-        lists[i].ids, lists[i].n_dev, A.rowptr, A.colors, S.chl.p, S.chh.p, S.nch.p);
+        lists[i].ids, lists[i].n_dev, A.rowptr, A.colors, A.dist == 1 ? DET_HEAVY : DET_HEAVY / 32, S.chl.p,
+        S.chh.p, S.nch.p);
     count_launch();
   }
-  FreeDet a{A.rowptr, A.col, A.colors, A.owned_flag, A.gids, A.deg, A.recolor_degrees, next, nnext, true};
-  k_free_heavy<<<num_sms() * 4, DET_HEAVY_THREADS, 0, s>>>(a, S.chh.p, S.nch.p + 1, conflicts);
-  k_free_light<<<grid_for(std::max<i64>(cap, 1) * 32, 256, num_sms() * 16), 256, 0, s>>>(a, S.chl.p, S.nch.p,
-                                                                                        conflicts);
-  count_launch(2);
+  FreeDet a{A.rowptr, A.col, A.colors, A.owned_flag, A.gids, A.deg, A.recolor_degrees, true, kr};
+  FREE_DET_DISPATCH(k_free_heavy, num_sms() * 4, DET_HEAVY_THREADS, a, S.chh.p, S.nch.p + 1, conflicts);
+  FREE_DET_DISPATCH(k_free_light, grid_for(std::max<i64>(cap, 1) * 32, 256, num_sms() * 16), 256, a, S.chl.p,
+                    S.nch.p, conflicts);
   CUDA_CHECK(cudaGetLastError());
 }
 

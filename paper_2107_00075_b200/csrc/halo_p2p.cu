@@ -9,9 +9,8 @@
 //
 //  * virtual ranks (one process): plain stores into the same colour array;
 //  * one rank per process: the owner stores the colour straight into the peer's
-//    ghost slot over NVLink (cudaIpc-mapped peer region) and raises the slot's flag
-//    there (plain byte store, no atomics); a flag barrier over peer memory then
-//    orders the stores before anyone's detection.  No NCCL launch, no pack/unpack,
+//    ghost slot over NVLink (cudaIpc-mapped peer region); a flag barrier over peer
+//    memory then orders the stores before anyone's detection.  No NCCL launch, no pack/unpack,
 //    no host round trip.  Round 0 (every boundary vertex changes) keeps the bulk
 //    NCCL send/recv path.
 // The reference's changed-only accounting (12 bytes per (vertex, destination) pair
@@ -32,7 +31,7 @@ __global__ void k_route_index(const i32* routed, i64 n, i32* idx) {
 // virtual ranks: worklist vertex -> its ghost copies (same array) + changed flags
 __global__ void k_xchg_local_list(const i32* wl, const i64* nwl_dev, const i32* route_idx, const i64* st_off,
                                   const i32* st_dst, const i32* st_pair, i32* colors, i32* last_sent,
-                                  unsigned long long* pair_cnt, uint8_t* gflag) {
+                                  unsigned long long* pair_cnt) {
   const i64 n = *nwl_dev;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 v = wl[i];
@@ -44,7 +43,6 @@ __global__ void k_xchg_local_list(const i32* wl, const i64* nwl_dev, const i32* 
     for (i64 t = st_off[r]; t < st_off[r + 1]; t++) {
       const i32 d = st_dst[t];
       colors[d] = c;
-      gflag[d] = 1;
       if (send) atomicAdd(&pair_cnt[st_pair[t]], 1ull);
     }
   }
@@ -53,7 +51,7 @@ __global__ void k_xchg_local_list(const i32* wl, const i64* nwl_dev, const i32* 
 // one rank per process: worklist vertex -> peers' ghost slots over NVLink
 __global__ void k_xchg_p2p(const i32* wl, const i64* nwl_dev, i64 lid_off, const i64* rs_off, const i32* rs_peer,
                            const i32* rs_rlid, i32* rs_last, const i32* colors, i32* const* peer_colors,
-                           uint8_t* const* peer_flag, unsigned long long* pair_cnt) {
+                           unsigned long long* pair_cnt) {
   const i64 n = *nwl_dev;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 v = wl[i];
@@ -66,16 +64,15 @@ __global__ void k_xchg_p2p(const i32* wl, const i64* nwl_dev, i64 lid_off, const
         atomicAdd(&pair_cnt[p], 1ull);
       }
       peer_colors[p][r] = c;
-      peer_flag[p][r] = 1;
     }
   }
   __threadfence_system();
 }
 
 // owned losers of the detection -> colour 0 in every ghost copy (virtual ranks)
-__global__ void k_zero_local(const i32* list, const unsigned long long* n_dev, const i32* route_idx,
-                             const i64* st_off, const i32* st_dst, i32* colors) {
-  const i64 n = (i64)*n_dev;
+__global__ void k_zero_local(const i32* list, const i64* n_dev, const i32* route_idx, const i64* st_off,
+                             const i32* st_dst, i32* colors) {
+  const i64 n = *n_dev;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 r = route_idx[list[i]];
     if (r < 0) continue;
@@ -85,9 +82,9 @@ __global__ void k_zero_local(const i32* list, const unsigned long long* n_dev, c
 
 // ... and over NVLink (the next NCCL allreduce orders these stores before anyone
 // colours again)
-__global__ void k_zero_p2p(const i32* list, const unsigned long long* n_dev, i64 lid_off, const i64* rs_off,
-                           const i32* rs_peer, const i32* rs_rlid, i32* const* peer_colors) {
-  const i64 n = (i64)*n_dev;
+__global__ void k_zero_p2p(const i32* list, const i64* n_dev, i64 lid_off, const i64* rs_off, const i32* rs_peer,
+                           const i32* rs_rlid, i32* const* peer_colors) {
+  const i64 n = *n_dev;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i64 o = list[i] - lid_off;
     for (i64 e = rs_off[o]; e < rs_off[o + 1]; e++) peer_colors[rs_peer[e]][rs_rlid[e]] = 0;
@@ -115,6 +112,12 @@ __global__ void k_init_rs_last(const i64* rs_off, i64 owned, i64 lid_off, const 
   }
 }
 
+// virtual ranks: ghost lid -> owner lid (same array)
+__global__ void k_kill_routes(const i32* routed, i64 nrouted, const i64* st_off, const i32* st_dst, i32* owner_lid) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nrouted; i += (i64)gridDim.x * blockDim.x)
+    for (i64 t = st_off[i]; t < st_off[i + 1]; t++) owner_lid[st_dst[t]] = routed[i];
+}
+
 __global__ void k_clear_flags(const i32* list, const i64* n_dev, uint8_t* flags) {
   const i64 n = *n_dev;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
@@ -134,27 +137,52 @@ void halo_route_index(World& w) {
     k_route_index<<<G(w.nrouted), 256, 0, s>>>(w.routed.p, w.nrouted, w.route_idx.p);
     count_launch();
   }
-  w.glist.alloc(std::max<i64>(w.NGHOST, 1), s);
-  w.gcnt.alloc(1, s);
-  w.gcnt.zero(s);
   if (!w.p2p) {
+    // kill routes of virtual ranks: every ghost's owner entry lives in this array
+    w.kill_lid.alloc(w.NL + 1, s);
+    w.kill_rank.alloc(w.NL + 1, s);
+    launch_fill_i32(w.kill_lid.p, w.NL + 1, -1, s);
+    launch_fill_i32(w.kill_rank.p, w.NL + 1, -1, s);
+    if (w.nrouted) {
+      k_kill_routes<<<G(w.nrouted), 256, 0, s>>>(w.routed.p, w.nrouted, w.st_off.p, w.st_dst.p, w.kill_lid.p);
+      count_launch();
+    }
     w.gflag.alloc(w.NL + 1, s);
     w.gflag.zero(s);
   }
 }
 
-// changed ghost lids since the last call (ascending), flags cleared
-void halo_changed_ghosts(World& w) {
+// the owned vertices flagged as losers since the last call (ascending) -> out,
+// count -> *n_out (device); flags cleared
+void halo_next_worklist(World& w, i32* out, i64* n_out) {
   cudaStream_t s = w.stream;
-  i64* cnt = reinterpret_cast<i64*>(w.gcnt.p);
   if (w.p2p) {
     const RankMeta& m = w.ranks[0];
-    select_flagged_base(w.my_flag + m.lid_off + m.owned, m.ghost, (i32)(m.lid_off + m.owned), w.glist.p, cnt, s);
-    k_clear_flags<<<G(m.ghost), 256, 0, s>>>(w.glist.p, cnt, w.my_flag);
+    select_flagged_base(w.my_flag + m.lid_off, m.owned, (i32)m.lid_off, out, n_out, s);
+    k_clear_flags<<<G(m.owned), 256, 0, s>>>(out, n_out, w.my_flag);
   } else {
-    select_flagged_base(w.gflag.p, w.NL, 0, w.glist.p, cnt, s);
-    k_clear_flags<<<G(w.NGHOST), 256, 0, s>>>(w.glist.p, cnt, w.gflag.p);
+    select_flagged_base(w.gflag.p, w.NL, 0, out, n_out, s);
+    k_clear_flags<<<G(w.NL), 256, 0, s>>>(out, n_out, w.gflag.p);
   }
+  count_launch();
+  CUDA_CHECK(cudaGetLastError());
+}
+
+KillRoute halo_kill_route(World& w) {
+  KillRoute kr;
+  kr.owner_lid = w.kill_lid.p;
+  kr.owner_rank = w.kill_rank.p;
+  kr.peer_colors = w.p2p ? w.peer_colors.p : nullptr;
+  kr.peer_flag = w.p2p ? w.peer_flag.p : nullptr;
+  kr.flags = w.p2p ? w.my_flag : w.gflag.p;
+  return kr;
+}
+
+// all ranks have finished their kills (stores into peers are fenced by the barrier)
+void halo_barrier(World& w) {
+  if (!w.p2p) return;
+  w.bar_epoch += (unsigned long long)(w.P - 1);
+  k_p2p_barrier<<<1, 32, 0, w.stream>>>(w.peer_ctrl.p, w.my_ctrl, w.P, w.my_rank, w.bar_epoch);
   count_launch();
   CUDA_CHECK(cudaGetLastError());
 }
@@ -162,8 +190,7 @@ void halo_changed_ghosts(World& w) {
 void halo_exchange_local_list(World& w, const i32* wl, const i64* nwl_dev, i64 nwl_max) {
   if (w.nrouted == 0 || nwl_max <= 0) return;
   k_xchg_local_list<<<G(nwl_max), 256, 0, w.stream>>>(wl, nwl_dev, w.route_idx.p, w.st_off.p, w.st_dst.p,
-                                                       w.st_pair.p, w.colors.p, w.last_sent.p, w.pair_cnt.p,
-                                                       w.gflag.p);
+                                                       w.st_pair.p, w.colors.p, w.last_sent.p, w.pair_cnt.p);
   count_launch();
   CUDA_CHECK(cudaGetLastError());
 }
@@ -172,16 +199,14 @@ void halo_exchange_p2p(World& w, const i32* wl, const i64* nwl_dev, i64 nwl_max)
   cudaStream_t s = w.stream;
   if (nwl_max > 0 && w.nsend > 0) {
     k_xchg_p2p<<<G(nwl_max), 256, 0, s>>>(wl, nwl_dev, w.ranks[0].lid_off, w.rs_off.p, w.rs_peer.p, w.rs_rlid.p,
-                                          w.rs_last.p, w.colors.p, w.peer_colors.p, w.peer_flag.p, w.pair_cnt.p);
+                                          w.rs_last.p, w.colors.p, w.peer_colors.p, w.pair_cnt.p);
     count_launch();
   }
-  w.bar_epoch += (unsigned long long)(w.P - 1);
-  k_p2p_barrier<<<1, 32, 0, s>>>(w.peer_ctrl.p, w.my_ctrl, w.P, w.my_rank, w.bar_epoch);
-  count_launch();
   CUDA_CHECK(cudaGetLastError());
+  halo_barrier(w);
 }
 
-void halo_broadcast_losers(World& w, const i32* list, const unsigned long long* n_dev, i64 n_max) {
+void halo_broadcast_losers(World& w, const i32* list, const i64* n_dev, i64 n_max) {
   if (n_max <= 0) return;
   cudaStream_t s = w.stream;
   if (w.p2p) {
@@ -303,6 +328,38 @@ void halo_setup_p2p(World& w, const std::vector<i32>& send_lids_abs, const std::
     CUDA_CHECK(cudaMemcpyAsync(rlid.data(), rlid_dev.p, sizeof(i32) * std::max<i64>(w.nsend, 1),
                                cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  // 5b. owner lids of my ghosts: peer p's send lids for me, in my receive order
+  std::vector<i32> olid((size_t)std::max<i64>(w.nrecv, 1));
+  {
+    DBuf<i32> sl_dev, ol_dev;
+    std::vector<i32> sl_local((size_t)std::max<i64>(w.nsend, 1));
+    for (i64 k = 0; k < w.nsend; k++) sl_local[(size_t)k] = (i32)(send_lids_abs[(size_t)k] - m.lid_off);
+    sl_dev.upload(sl_local.data(), std::max<i64>(w.nsend, 1), s);
+    ol_dev.alloc(std::max<i64>(w.nrecv, 1), s);
+    if (!NCCL_OK(ncclGroupStart())) throw Error(CHROMA_ECUDA, "ncclGroupStart failed");
+    for (i32 p = 0; p < P; p++) {
+      if (p == me) continue;
+      if (w.send_cnt[(size_t)p])
+        ncclSend(sl_dev.p + w.send_off[(size_t)p], w.send_cnt[(size_t)p], ncclInt32, p, w.comm, s);
+      if (w.recv_cnt[(size_t)p])
+        ncclRecv(ol_dev.p + w.recv_off[(size_t)p], w.recv_cnt[(size_t)p], ncclInt32, p, w.comm, s);
+    }
+    if (!NCCL_OK(ncclGroupEnd())) throw Error(CHROMA_ECUDA, "owner lid exchange failed");
+    CUDA_CHECK(cudaMemcpyAsync(olid.data(), ol_dev.p, sizeof(i32) * std::max<i64>(w.nrecv, 1),
+                               cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  {
+    std::vector<i32> kl((size_t)(w.NL + 1), -1), kp((size_t)(w.NL + 1), -1);
+    for (i32 p = 0; p < P; p++)
+      for (i64 k = w.recv_off[(size_t)p]; k < w.recv_off[(size_t)p + 1]; k++) {
+        const i64 g = recv_lids_abs[(size_t)k];
+        kl[(size_t)g] = olid[(size_t)k];
+        kp[(size_t)g] = p;
+      }
+    w.kill_lid.upload(kl.data(), w.NL + 1, s);
+    w.kill_rank.upload(kp.data(), w.NL + 1, s);
   }
   // 6. send entries grouped by owned lid (counting sort)
   std::vector<i64> off((size_t)m.owned + 1, 0);

@@ -121,17 +121,26 @@ struct DetectScratch {
   DBuf<unsigned long long> nch;
   bool prev_valid = false;
 };
-// Free-running D1 detection around explicit changed-vertex lists (device counts):
-// pairs with a ghost end and equal non-zero colours uncolour their loser; owned
-// losers are appended to next[*nnext].  Adds the number uncoloured to *conflicts.
+// Free-running detection around explicit changed-vertex lists (device counts).
+// Every pair with one owned end, one ghost end and equal non-zero colours
+// uncolours its loser at the loser's owner -- locally, or through KillRoute for a
+// ghost: the owner's lid in this process's colour array (virtual ranks, peer =
+// -1) or in peer `owner_rank`'s NVLink-mapped array -- and raises the owner's
+// loser flag.  Adds the number of vertices uncoloured to *conflicts.
 struct FreeList {
   const i32* ids;
   const unsigned long long* n_dev;
   i64 cap;
 };
-void run_detect_free_lists(const DetectArgs& A, i64 nv, const FreeList* lists, int nlists, i32* next,
-                           unsigned long long* nnext, DetectScratch& S, unsigned long long* conflicts,
-                           cudaStream_t s);
+struct KillRoute {
+  const i32* owner_lid = nullptr;    // per lid: owner's lid of a ghost, -1 for owned
+  const i32* owner_rank = nullptr;   // per lid: owner process rank (NVLink), -1 = this array
+  i32* const* peer_colors = nullptr;
+  uint8_t* const* peer_flag = nullptr;
+  uint8_t* flags = nullptr;          // this process's loser flags (per lid)
+};
+void run_detect_free_lists(const DetectArgs& A, i64 nv, const FreeList* lists, int nlists, const KillRoute& kr,
+                           DetectScratch& S, unsigned long long* conflicts, cudaStream_t s);
 // Adds the number of conflicts to *conflicts_dev (device, unsigned long long).
 void run_detect(const DetectArgs& a, i64 num_vertices, DetectScratch& S,
                 unsigned long long* conflicts_dev, cudaStream_t s);

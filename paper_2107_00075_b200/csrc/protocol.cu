@@ -348,18 +348,19 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   w.cs.flags.reserve(w.NL + 1, s);
   const i64 nstats = 3 + w.P;  // allreduced; hs[nstats] is this process's next-worklist size
   std::vector<unsigned long long> hs((size_t)nstats + 1);
-  // Free-running distance-1 fast path: after round 0 the worklist is the owned
-  // losers the detection appended, the exchange walks only that worklist (NVLink
-  // peer stores between processes), and the detection only the pairs around
-  // vertices that changed (worklist + changed ghost copies).
+  // Free-running fast path (all modes): after round 0 the worklist is the owned
+  // losers flagged by any rank's detection, the exchange walks only that worklist
+  // (NVLink peer stores between processes), and the detection only the recoloured
+  // owned vertices' sets, uncolouring each loser at its owner (halo_p2p.cu).
   static const bool no_fast = std::getenv("CHROMA_NO_FAST_FREE") != nullptr;
-  const bool fast = algo == CHROMA_ALGO_FREE && dist == 1 && !no_fast && (!w.connected || w.p2p || w.P == 1);
+  const bool fast = algo == CHROMA_ALGO_FREE && !no_fast && (!w.connected || w.p2p || w.P == 1);
   if (fast) {
     halo_route_index(w);
     w.next_wl.reserve(w.NL + 1, s);
-    w.nghost_dev.reserve(1, s);
-    const unsigned long long ng = (unsigned long long)w.NGHOST;
-    CUDA_CHECK(cudaMemcpyAsync(w.nghost_dev.p, &ng, sizeof(ng), cudaMemcpyHostToDevice, s));
+    w.nghost_dev.reserve(2, s);
+    const unsigned long long ng[2] = {(unsigned long long)w.NGHOST, (unsigned long long)w.NB2};
+    CUDA_CHECK(cudaMemcpyAsync(w.nghost_dev.p, ng, sizeof(ng), cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
   }
   i64 nwl_host = w.NL;
   cudaEvent_t ev[8];
@@ -396,9 +397,8 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     CUDA_CHECK(cudaMemsetAsync(w.stats.p, 0, sizeof(unsigned long long) * (nstats + 1), s));
     CUDA_CHECK(cudaEventRecord(ev[0], s));
     if (fast && round > 0) {
-      // the previous detection's owned losers, ascending (the ordered kernel needs it)
+      // the previous detection's owned losers, ascending
       nwl_host = (i64)hs[(size_t)nstats];
-      sort_i32(w.next_wl.p, nwl_host, s);
       CUDA_CHECK(cudaMemcpyAsync(w.cs.wl.p, w.next_wl.p, sizeof(i32) * std::max<i64>(nwl_host, 1),
                                  cudaMemcpyDeviceToDevice, s));
       CUDA_CHECK(cudaMemcpyAsync(w.cs.nwl.p, &hs[(size_t)nstats], sizeof(i64), cudaMemcpyHostToDevice, s));
@@ -438,19 +438,23 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     if (fast && w.NGHOST == 0) {
       // no cut edges: a locally proper colouring is final
     } else if (fast) {
-      // every cut pair sits in a ghost row, so when every vertex changed (round 0)
-      // the ghost rows alone cover the scan; later rounds add the recoloured owned rows
-      FreeList lists[2];
-      int nl = 0;
+      // Round 0 (every vertex changed): one side of each cut pair suffices -- the
+      // ghost rows for D1 (every cut edge is in one; rows hold local edges only), the
+      // owned boundary_d2 rows for D2/PD2.  Later rounds: a conflicting pair always
+      // has a recoloured end, and that end's owner finds it, so only the worklist
+      // is walked.  Losers are uncoloured at their owners (NVLink for peers).
+      FreeList list;
       if (!listed) {
-        lists[nl++] = {w.ghosts.p, w.nghost_dev.p, w.NGHOST};
+        if (d2) list = {w.b2.p, w.nghost_dev.p + 1, w.NB2};
+        else list = {w.ghosts.p, w.nghost_dev.p, w.NGHOST};
       } else {
-        lists[nl++] = {w.cs.wl.p, reinterpret_cast<const unsigned long long*>(w.cs.nwl.p), nwl_host};
-        halo_changed_ghosts(w);  // flags raised by this round's exchange
-        lists[nl++] = {w.glist.p, w.gcnt.p, w.NGHOST};
+        list = {w.cs.wl.p, reinterpret_cast<const unsigned long long*>(w.cs.nwl.p), nwl_host};
       }
-      run_detect_free_lists(da, w.NL, lists, nl, w.next_wl.p, w.stats.p + nstats, w.det, w.stats.p, s);
-      halo_broadcast_losers(w, w.next_wl.p, w.stats.p + nstats, w.NL);
+      run_detect_free_lists(da, w.NL, &list, 1, halo_kill_route(w), w.det, w.stats.p, s);
+      halo_barrier(w);  // every rank's kills have landed
+      i64* next_cnt = reinterpret_cast<i64*>(w.stats.p + nstats);
+      halo_next_worklist(w, w.next_wl.p, next_cnt);
+      halo_broadcast_losers(w, w.next_wl.p, next_cnt, w.NL);
     } else {
       run_detect(da, w.NL, w.det, w.stats.p, s);
     }

@@ -79,7 +79,7 @@ struct World {
   void* ipc_base = nullptr;                 // own region (cudaMalloc)
   std::vector<void*> peer_base;             // opened peer regions (nullptr for self)
   unsigned long long* my_ctrl = nullptr;    // [1] barrier arrivals
-  uint8_t* my_flag = nullptr;               // changed flag per lid (written by peers)
+  uint8_t* my_flag = nullptr;               // loser flag per lid (raised by any rank's detection)
   DBuf<i32*> peer_colors;                   // device arrays [P]
   DBuf<uint8_t*> peer_flag;
   DBuf<unsigned long long*> peer_ctrl;
@@ -89,9 +89,8 @@ struct World {
   std::vector<unsigned long long> route_pair_static;  // routes per (src,dst) pair
   // virtual worlds: owned lid -> routed index (-1: not routed), built lazily
   DBuf<i32> route_idx;
-  DBuf<i32> glist;                          // changed ghost lids of this round
-  DBuf<unsigned long long> gcnt;
-  DBuf<uint8_t> gflag;                      // changed flag per lid (virtual worlds)
+  DBuf<uint8_t> gflag;                      // loser flag per lid (virtual worlds)
+  DBuf<i32> kill_lid, kill_rank;            // per ghost lid: owner's lid / owner process (-1: here)
   DBuf<i32> next_wl;                        // owned losers of the last detection
   DBuf<unsigned long long> nghost_dev;      // NGHOST on the device (round-0 changed list)
   // protocol scratch
@@ -120,9 +119,11 @@ void halo_route_index(World& w);
 void halo_exchange_local_list(World& w, const i32* wl, const i64* nwl_dev, i64 nwl_max);
 void halo_exchange_p2p(World& w, const i32* wl, const i64* nwl_dev, i64 nwl_max);
 void halo_init_p2p_last(World& w);
-void halo_changed_ghosts(World& w);  // -> w.glist / w.gcnt (ascending), flags cleared
+void halo_next_worklist(World& w, i32* out, i64* n_out);  // flagged owned losers, ascending
+KillRoute halo_kill_route(World& w);
+void halo_barrier(World& w);  // all ranks' peer stores visible (no-op without NVLink peers)
 // detection's owned losers -> 0 in every ghost copy (owners are the only writers)
-void halo_broadcast_losers(World& w, const i32* list, const unsigned long long* n_dev, i64 n_max);
+void halo_broadcast_losers(World& w, const i32* list, const i64* n_dev, i64 n_max);
 void halo_setup_p2p(World& w, const std::vector<i32>& send_lids_abs, const std::vector<i32>& send_peer,
                     const std::vector<i32>& recv_lids_abs);
 void halo_release_p2p(World& w);

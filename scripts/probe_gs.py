@@ -86,3 +86,22 @@ if "c3trace" in which:
     print("max degree", int(np.diff(g.row_offsets).max()), "heavy>1024", int((np.diff(g.row_offsets) > 1024).sum()),
           ">4096", int((np.diff(g.row_offsets) > 4096).sum()), flush=True)
     run(f"rmat s{sc} free", g, "d1", algorithm="free", check=False, reps=2)
+if "table" in which:
+    run("C1 grid 1000^2 gs", G.gen_hex_mesh(1000, 1000, 1), "d1")
+    run("C2 27pt 128^3 gs", G.gen_stencil27(128, device="cuda"), "d1-2gl")
+    run("C2 27pt 128^3 gs P8", G.gen_stencil27(128, device="cuda"), "d1-2gl", P=8)
+    run("R-MAT s20 gs", G.gen_rmat(20, 16, 1, device="cuda"), "d1")
+    run("R-MAT s20 free", G.gen_rmat(20, 16, 1, device="cuda"), "d1", algorithm="free")
+    run("C4 7pt 200^3 d2 gs", G.gen_hex_mesh(200, 200, 200), "d2", check=False)
+    run("C4 7pt 200^3 d2 free", G.gen_hex_mesh(200, 200, 200), "d2", check=False, algorithm="free")
+    run("C4 7pt 200^3 d2 gs P8", G.gen_hex_mesh(200, 200, 200), "d2", check=False, P=8)
+    run("C5 pd2 2^20 gs", G.gen_random_bipartite(1 << 20, 32, 3, device="cuda").graph, "pd2", check=False)
+    run("C5 pd2 2^20 free", G.gen_random_bipartite(1 << 20, 32, 3, device="cuda").graph, "pd2", check=False, algorithm="free")
+    run("C5 pd2 2^22 free", G.gen_random_bipartite(1 << 22, 32, 3, device="cuda").graph, "pd2", check=False, algorithm="free")
+    run("C5 pd2 2^22 free P8", G.gen_random_bipartite(1 << 22, 32, 3, device="cuda").graph, "pd2", check=False, algorithm="free", P=8)
+if "d2free" in which:
+    run("C4 7pt 200^3 d2 free", G.gen_hex_mesh(200, 200, 200), "d2", check=False, algorithm="free")
+    run("C4 7pt 200^3 d2 free P8", G.gen_hex_mesh(200, 200, 200), "d2", check=False, algorithm="free", P=8)
+    run("7pt 100^3 d2 free P8", G.gen_hex_mesh(100, 100, 100), "d2", algorithm="free", P=8)
+    run("pd2 2^18 free P8", G.gen_random_bipartite(1 << 18, 32, 3, device="cuda").graph, "pd2", algorithm="free", P=8)
+    run("C5 pd2 2^22 free P8", G.gen_random_bipartite(1 << 22, 32, 3, device="cuda").graph, "pd2", check=False, algorithm="free", P=8)
