@@ -342,7 +342,7 @@ def main():
     if N == 1 and wl.name == "c2" and args.L == 128 and wl.algorithm == "gauss-seidel":
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-                traffic = json.load(fh)["gs_kernel_c2_p1"]["dram_bytes_per_launch"]
+                traffic = json.load(fh)["gs_d1_kernel_c2_p1"]["dram_bytes_per_launch"]
         except Exception:
             traffic = None
     # ---- end to end through the public API with host buffers
