@@ -44,6 +44,8 @@ struct D1Args {
   i64 wl_base;
   const i64* nwl;
   unsigned long long* ticket;
+  bool level_mode;  // wl is a level schedule (gs_levels.cu): no in-chunk dependencies,
+                    // -1 entries pad levels to whole chunks
 };
 
 struct D1Smem {
@@ -114,10 +116,12 @@ __global__ void __launch_bounds__(WARPS * 32) gs_d1_kernel(D1Args a) {
     const i64 chunk = (i64)__shfl_sync(FULL, t, 0);
     if (chunk >= nchunks) break;
     const i64 idx = chunk * 32 + lane;
-    const bool act = idx < nwl;
-    const i32 v = act ? (a.wl ? a.wl[idx] : (i32)(a.wl_base + idx)) : INT32_MAX;
+    i32 v = idx < nwl ? (a.wl ? a.wl[idx] : (i32)(a.wl_base + idx)) : -1;
+    const bool act = v >= 0;
+    if (!act) v = INT32_MAX;
     sm.v[lane] = v;
-    const i32 kfirst = __shfl_sync(FULL, v, 0);
+    // level schedule: every smaller neighbour is external (claimed in an earlier chunk)
+    const i32 kfirst = a.level_mode ? v : __shfl_sync(FULL, v, 0);
     const i64 rs = act ? a.rowptr[v] : 0, re = act ? a.rowptr[v + 1] : 0;
     const bool heavy = act && re - rs > HEAVY;
     i64 p0 = rs, p1 = rs;
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(WARPS * 32) gs_d1_kernel(D1Args a) {
     }
     __syncwarp();
     // in-chunk predecessors: worklist members of [kfirst, v) are chunk lanes
-    if (act && !heavy) {
+    if (act && !heavy && !a.level_mode) {
       for (i64 i = p0; i < p1; i++) {
         const i32 u = a.col[i];
         int lo = 0;  // lane holding u (sm.v is ascending; inactive lanes hold INT32_MAX)
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(WARPS * 32) gs_d1_kernel(D1Args a) {
       }
     }
     // heavy rows: the warp computes splits and the in-chunk mask cooperatively
-    u32 hv = __ballot_sync(FULL, heavy);
+    u32 hv = __ballot_sync(FULL, heavy && !a.level_mode);
     while (hv) {
       const int l = __ffs(hv) - 1;
       hv &= hv - 1;
@@ -226,7 +230,8 @@ __global__ void __launch_bounds__(WARPS * 32) gs_d1_kernel(D1Args a) {
         for (int w = 0; w < WORDS; w++) mm[w] = 0;
         int pend = 0;
         i32 sent = -1;
-        scan_row(a, a.rowptr[vl] + lane, a.rowptr[vl + 1], 32, kfirst, vl, mm, pend, sent, nullptr);
+        scan_row(a, a.rowptr[vl] + lane, a.rowptr[vl + 1], 32, a.level_mode ? vl : kfirst, vl, mm, pend, sent,
+                 nullptr);
         pend = __reduce_add_sync(FULL, pend);
         sent = __reduce_max_sync(FULL, sent);
 #pragma unroll
@@ -329,6 +334,7 @@ bool launch_gs_d1(const GsLaunch& L, cudaStream_t s) {
   a.wl_base = L.wl_base;
   a.nwl = L.nwl_dev;
   a.ticket = L.ticket;
+  a.level_mode = L.level_mode;
   CUDA_CHECK(cudaMemsetAsync(L.ticket, 0, sizeof(unsigned long long), s));
   const i64 nchunks = (L.nwl_max + 31) / 32;
   static const int bps_env = std::getenv("CHROMA_GS_BPS") ? std::atoi(std::getenv("CHROMA_GS_BPS")) : 0;

@@ -23,6 +23,7 @@ struct GsLaunch {
   int dist = 1;
   bool partial = false;
   i64 nv = 0;                  // number of vertices (ids are < nv)
+  bool level_mode = false;     // wl is a padded level schedule (gs_levels.cu), D1 only
 };
 void launch_gs(const GsLaunch& L, cudaStream_t s);
 bool launch_gs_d1(const GsLaunch& L, cudaStream_t s);  // false if not applicable

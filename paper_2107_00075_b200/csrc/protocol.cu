@@ -227,6 +227,15 @@ gauss_seidel:
     L.dist = dist;
     L.partial = partial;
     L.nv = nv;
+    if (S.level_wl && dist == 1) {
+      // same vertex set, claimed level by level or rank-interleaved (gs_levels.cu)
+      S.level_n_dev.reserve(1, s);
+      CUDA_CHECK(cudaMemcpyAsync(S.level_n_dev.p, &S.level_n, sizeof(i64), cudaMemcpyHostToDevice, s));
+      L.wl = S.level_wl;
+      L.nwl_dev = S.level_n_dev.p;
+      L.nwl_max = S.level_n;
+      L.level_mode = S.level_mode;
+    }
     if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
     launch_gs(L, s);
     if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
@@ -353,6 +362,10 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   // (NVLink peer stores between processes), and the detection only the recoloured
   // owned vertices' sets, uncolouring each loser at its owner (halo_p2p.cu).
   static const bool no_fast = std::getenv("CHROMA_NO_FAST_FREE") != nullptr;
+  static const bool no_levels = std::getenv("CHROMA_NO_LEVELS") != nullptr;
+  // round-0 schedule: 0 auto (levels if the DAG is wide, else rank-interleaved for
+  // virtual ranks, else id order), 1 levels only, 2 interleave only, 3 id order
+  static const int sched = (int)env_i64("CHROMA_GS_SCHEDULE", 0);
   const bool fast = algo == CHROMA_ALGO_FREE && !no_fast && (!w.connected || w.p2p || w.P == 1);
   if (fast) {
     halo_route_index(w);
@@ -415,8 +428,36 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
                                               w.rank_hi - w.rank_lo, w.stats.p);
     count_launch();
     const bool gs_like = algo != CHROMA_ALGO_JACOBI;
+    // round 0 colours every owned vertex: claim them by DAG level (cached per world)
+    w.cs.level_wl = nullptr;
+    if (round == 0 && dist == 1 && gs_like && !no_levels) {
+      if (w.level_n < 0) {
+        i64 owned = 0;
+        std::vector<i64> counts;
+        for (auto& m : w.ranks) {
+          owned += m.owned;
+          counts.push_back(m.owned);
+        }
+        i64 n = 0;
+        // levels when the DAG is wide; else (virtual ranks) rank-interleaved id order
+        w.level_mode = (sched == 0 || sched == 1) &&
+                       build_level_order(w.g.rowptr.p, w.g.col.p, w.NL, w.cs.wl.p, owned, w.level_wl, n, s);
+        w.level_n = w.level_mode ? n : 0;
+        if (!w.level_mode && (sched == 0 || sched == 2) &&
+            build_rank_interleave(w.cs.wl.p, counts, w.level_wl, n, s))
+          w.level_n = n;
+        // the colour array is untouched; restart the round's timing after the one-time build
+        CUDA_CHECK(cudaEventRecord(ev[0], s));
+      }
+      if (w.level_n > 0) {
+        w.cs.level_wl = w.level_wl.p;
+        w.cs.level_n = w.level_n;
+        w.cs.level_mode = w.level_mode;
+      }
+    }
     color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, nwl_host, true, dist, partial,
               algo, true, w.cs, s, gs_like ? ev[6] : nullptr, gs_like ? ev[7] : nullptr);
+    w.cs.level_wl = nullptr;
     CUDA_CHECK(cudaEventRecord(ev[1], s));
     // exchange: every ghost takes its owner's colour; accounting is changed-only
     const bool listed = fast && round > 0;  // exchange and detection driven by lists

@@ -34,6 +34,12 @@ struct ColorScratch {
   DBuf<uint8_t> flags, in_round;
   DBuf<unsigned long long> ticket;
   DBuf<i32> fl[6];  // free-running light/heavy/tiny lists x 2
+  // optional schedule for the next Gauss-Seidel launch (gs_levels.cu): a level
+  // schedule (level_mode) or a rank-interleaved id order
+  const i32* level_wl = nullptr;
+  i64 level_n = 0;
+  bool level_mode = true;
+  DBuf<i64> level_n_dev;
   DBuf<i64> fcnt;
   FreeWaveScratch fw;
 };
@@ -98,6 +104,10 @@ struct World {
   DetectScratch det;
   DBuf<unsigned long long> stats;  // [0] conflicts [1] bytes [2] msgs [3..3+P) recolored
   DBuf<i32> deg_override;
+  // schedule of the full owned worklist (computed on first use, -1 = not yet)
+  DBuf<i32> level_wl;
+  i64 level_n = -1;
+  bool level_mode = false;
   // device-side timing of the last run_distributed (CUDA events on `stream`)
   double t_total = 0, t_color_kernel = 0, t_color = 0, t_comm = 0, t_detect = 0;
 
@@ -127,6 +137,16 @@ void halo_broadcast_losers(World& w, const i32* list, const i64* n_dev, i64 n_ma
 void halo_setup_p2p(World& w, const std::vector<i32>& send_lids_abs, const std::vector<i32>& send_peer,
                     const std::vector<i32>& recv_lids_abs);
 void halo_release_p2p(World& w);
+
+// Level schedule of a sorted worklist (padded to chunks; false if the DAG is too
+// deep and narrow to benefit).  gs_levels.cu.
+bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl, i64 nwl, DBuf<i32>& out,
+                       i64& nout, cudaStream_t s);
+
+// Round-robin chunk order over the virtual ranks of a world (rank_counts = owned
+// vertices per rank, contiguous in wl).  gs_levels.cu.
+bool build_rank_interleave(const i32* wl, const std::vector<i64>& rank_counts, DBuf<i32>& out, i64& nout,
+                           cudaStream_t s);
 
 // Colour the worklist of a CSR (absolute vertex ids).  `wl_sorted_unique` skips the
 // device sort/dedupe for protocol worklists that are produced in order.

@@ -105,3 +105,11 @@ if "d2free" in which:
     run("7pt 100^3 d2 free P8", G.gen_hex_mesh(100, 100, 100), "d2", algorithm="free", P=8)
     run("pd2 2^18 free P8", G.gen_random_bipartite(1 << 18, 32, 3, device="cuda").graph, "pd2", algorithm="free", P=8)
     run("C5 pd2 2^22 free P8", G.gen_random_bipartite(1 << 22, 32, 3, device="cuda").graph, "pd2", check=False, algorithm="free", P=8)
+if "sched" in which:
+    run("C1 grid 1000^2 gs", G.gen_hex_mesh(1000, 1000, 1), "d1", check=False)
+    run("C2 27pt 128^3 gs", G.gen_stencil27(128, device="cuda"), "d1-2gl", check=False)
+    run("C2 27pt 128^3 gs P8", G.gen_stencil27(128, device="cuda"), "d1-2gl", P=8, check=False)
+    run("C2 27pt 128^3 gs P2", G.gen_stencil27(128, device="cuda"), "d1-2gl", P=2, check=False)
+    run("R-MAT s20 gs", G.gen_rmat(20, 16, 1, device="cuda"), "d1", check=False)
+    run("R-MAT s20 gs P8", G.gen_rmat(20, 16, 1, device="cuda"), "d1", check=False, P=8)
+    run("C1 grid 1000^2 gs P8", G.gen_hex_mesh(1000, 1000, 1), "d1", check=False, P=8)
