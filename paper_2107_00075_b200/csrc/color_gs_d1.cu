@@ -338,7 +338,11 @@ bool launch_gs_d1(const GsLaunch& L, cudaStream_t s) {
   CUDA_CHECK(cudaMemsetAsync(L.ticket, 0, sizeof(unsigned long long), s));
   const i64 nchunks = (L.nwl_max + 31) / 32;
   static const int bps_env = std::getenv("CHROMA_GS_BPS") ? std::atoi(std::getenv("CHROMA_GS_BPS")) : 0;
-  int grid = (int)std::min<i64>((nchunks + WARPS - 1) / WARPS, (i64)num_sms() * (bps_env > 0 ? bps_env : 16));
+  // id order needs a wide claim window (the wavefront spans the id range); a level
+  // schedule needs only a few levels in flight, and fewer pollers keep the
+  // critical-path warps issuing
+  const int bps = bps_env > 0 ? bps_env : (L.level_mode ? 2 : 16);
+  int grid = (int)std::min<i64>((nchunks + WARPS - 1) / WARPS, (i64)num_sms() * bps);
   if (grid < 1) grid = 1;
   gs_d1_kernel<<<grid, WARPS * 32, 0, s>>>(a);
   count_launch();

@@ -1,1 +1,3 @@
-for sc in 0 1 2 3; do echo "schedule=$sc"; CHROMA_LEVEL_TRACE=1 CHROMA_GS_SCHEDULE=$sc python scripts/probe_gs.py sched 2>&1 | grep -v "^\[levels\] [0-9]* levels" | cut -c1-160; done
+python scripts/probe_gs.py sched 2>&1 | cut -c1-150
+python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline | cut -c1-330
+python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
