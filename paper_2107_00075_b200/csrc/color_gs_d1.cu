@@ -46,6 +46,7 @@ struct D1Args {
   unsigned long long* ticket;
   bool level_mode;  // wl is a level schedule (gs_levels.cu): no in-chunk dependencies,
                     // -1 entries pad levels to whole chunks
+  bool poll_all;    // poll the whole pending list instead of the sentinel
 };
 
 struct D1Smem {
@@ -309,7 +310,13 @@ __global__ void __launch_bounds__(WARPS * 32) gs_d1_kernel(D1Args a) {
       if (done == FULL) break;
       // ---- poll sentinels (one load per waiting lane)
       need = false;
-      if (state == 0) need = sentinel < 0 || ld_relaxed(a.val + sentinel) != PENDING;
+      if (state == 0) {
+        // level schedule: re-check the whole (short) list each poll -- one batch of
+        // loads -- rather than waiting on the sentinel first: deps of one level
+        // commit in any order
+        if (a.poll_all && !heavy && npend > 0 && npend <= PL) need = true;
+        else need = sentinel < 0 || ld_relaxed(a.val + sentinel) != PENDING;
+      }
       if (__any_sync(FULL, need)) {
         ns = 32;
       } else {
@@ -335,6 +342,8 @@ bool launch_gs_d1(const GsLaunch& L, cudaStream_t s) {
   a.nwl = L.nwl_dev;
   a.ticket = L.ticket;
   a.level_mode = L.level_mode;
+  static const int poll_env = std::getenv("CHROMA_GS_POLL_ALL") ? std::atoi(std::getenv("CHROMA_GS_POLL_ALL")) : -1;
+  a.poll_all = poll_env >= 0 ? poll_env != 0 : L.level_mode;
   CUDA_CHECK(cudaMemsetAsync(L.ticket, 0, sizeof(unsigned long long), s));
   const i64 nchunks = (L.nwl_max + 31) / 32;
   static const int bps_env = std::getenv("CHROMA_GS_BPS") ? std::atoi(std::getenv("CHROMA_GS_BPS")) : 0;

@@ -1,3 +1,1 @@
-python scripts/probe_gs.py sched 2>&1 | cut -c1-150
-python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline | cut -c1-330
-python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
+for pa in 0 1; do echo "poll_all=$pa"; CHROMA_GS_POLL_ALL=$pa python scripts/probe_gs.py sched 2>&1 | cut -c1-150 | grep -v "R-MAT s20 gs P8"; done
