@@ -54,12 +54,20 @@ __global__ void k_level_indeg(const i64* rowptr, const i32* col, const i32* wl, 
   }
 }
 
-// release the successors of one frontier; warp per vertex (rows may be long)
+// release the successors of one frontier; warp per vertex (rows may be long).
+// Counters rotate over three slots so one launch per level suffices: this level's
+// size is cnt[l%3] (recorded into sizes[l]), the next one accumulates in
+// cnt[(l+1)%3], and cnt[(l+2)%3] is cleared for the level after.
 __global__ void k_level_step(const i64* rowptr, const i32* col, const uint8_t* member, const i32* frontier,
-                             const unsigned long long* nfront_dev, i32 lvl, i32* indeg, i32* level, i32* next,
-                             unsigned long long* nnext) {
+                             unsigned long long* cnt, i64 lvl, i32* indeg, i32* level, i32* next,
+                             unsigned long long* sizes) {
   const int lane = threadIdx.x & 31;
-  const i64 n = (i64)*nfront_dev;
+  const i64 n = (i64)cnt[lvl % 3];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sizes[lvl] = (unsigned long long)n;
+    cnt[(lvl + 2) % 3] = 0;
+  }
+  unsigned long long* nnext = cnt + (lvl + 1) % 3;
   const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
   for (i64 i = warp; i < n; i += nwarps) {
@@ -69,7 +77,7 @@ __global__ void k_level_step(const i64* rowptr, const i32* col, const uint8_t* m
       const i32 x = col[e];
       if (x <= v) break;  // rows are sorted: only successors (x > v) from the top
       if (member[x] && atomicSub(indeg + x, 1) == 1) {
-        level[x] = lvl + 1;
+        level[x] = (i32)lvl + 1;
         next[atomicAdd(nnext, 1ull)] = x;
       }
     }
@@ -118,37 +126,48 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   level.alloc(nv + 1, s);
   fa.alloc(nwl, s);
   fb.alloc(nwl, s);
-  cnt.alloc(2, s);
+  cnt.alloc(3, s);
   cnt.zero(s);
   k_mark_members<<<G(nwl), 256, 0, s>>>(wl, nwl, member.p);
   k_level_indeg<<<grid_for(nwl, 256, num_sms() * 8), 256, 0, s>>>(rowptr, col, wl, nwl, member.p, indeg.p,
                                                                    level.p, fa.p, cnt.p);
   count_launch(2);
-  std::vector<i64> sizes;
-  unsigned long long c = 0;
-  CUDA_CHECK(cudaMemcpyAsync(&c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  i32* cur = fa.p;
-  i32* nxt = fb.p;
-  int p = 0;
-  i64 seen = 0;
-  while (c > 0) {
-    sizes.push_back((i64)c);
-    seen += (i64)c;
-    if ((i64)sizes.size() > max_levels) {  // deep and narrow: id order is better
+  // frontier sizes land in a device array; the host checks every BATCH levels
+  constexpr int BATCH = 64;
+  const i64 cap_levels = max_levels + BATCH + 1;
+  DBuf<unsigned long long> dsz;
+  dsz.alloc(cap_levels + 1, s);
+  dsz.zero(s);
+  std::vector<unsigned long long> hsz((size_t)cap_levels + 1, 0);
+  i32* buf[2] = {fa.p, fb.p};
+  CUDA_CHECK(cudaMemsetAsync(cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
+  i64 lvl = 0;
+  bool done = false;
+  const int grid = num_sms() * 8;
+  while (!done) {
+    for (int k = 0; k < BATCH; k++, lvl++) {
+      const int p = (int)(lvl & 1);
+      k_level_step<<<grid, 256, 0, s>>>(rowptr, col, member.p, buf[p], cnt.p, lvl, indeg.p, level.p, buf[p ^ 1],
+                                        dsz.p);
+    }
+    count_launch(BATCH);
+    CUDA_CHECK(cudaMemcpyAsync(hsz.data(), dsz.p, sizeof(unsigned long long) * (size_t)lvl, cudaMemcpyDeviceToHost,
+                               s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    done = hsz[(size_t)lvl - 1] == 0;
+    if (!done && lvl > max_levels) {  // deep and narrow: id order is better
       if (trace) std::fprintf(stderr, "[levels] > %lld levels for %lld vertices: id order\n", (long long)max_levels,
                               (long long)nwl);
       return false;
     }
-    CUDA_CHECK(cudaMemsetAsync(cnt.p + (p ^ 1), 0, sizeof(unsigned long long), s));
-    k_level_step<<<grid_for((i64)c * 32, 256, num_sms() * 16), 256, 0, s>>>(
-        rowptr, col, member.p, cur, cnt.p + p, (i32)sizes.size() - 1, indeg.p, level.p, nxt, cnt.p + (p ^ 1));
-    count_launch();
-    CUDA_CHECK(cudaMemcpyAsync(&c, cnt.p + (p ^ 1), sizeof(c), cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    std::swap(cur, nxt);
-    p ^= 1;
   }
+  std::vector<i64> sizes;
+  i64 seen = 0;
+  for (i64 l = 0; l < lvl && hsz[(size_t)l] > 0; l++) {
+    sizes.push_back((i64)hsz[(size_t)l]);
+    seen += (i64)hsz[(size_t)l];
+  }
+  if ((i64)sizes.size() > max_levels) return false;
   CHROMA_REQUIRE(seen == nwl, CHROMA_ERUNTIME, "level schedule did not cover the worklist");
   const i64 L = (i64)sizes.size();
   if (trace) std::fprintf(stderr, "[levels] %lld levels for %lld vertices\n", (long long)L, (long long)nwl);
