@@ -149,6 +149,68 @@ __global__ void __launch_bounds__(1024) k_resolve(const int2* ev, i64 E, uint8_t
   if (t == 0) *conflicts += fired_count;
 }
 
+// Grid-wide form of k_resolve for large event lists (cooperative launch, one
+// 1024-thread CTA per SM): the same Jacobi fixed point over the event order, every
+// sweep spread over the whole GPU with software grid barriers.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nb - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024, 1) k_resolve_grid(const int2* ev, i64 E, uint8_t* fired, i32* kill,
+                                                          i32* colors, unsigned long long* conflicts, unsigned* bar,
+                                                          int* changed) {
+  const i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x, T = (i64)gridDim.x * blockDim.x;
+  const unsigned nb = gridDim.x;
+  for (i64 e = t; e < E; e += T) fired[e] = 1;
+  for (i64 it = 0; it <= E + 1; it++) {
+    // three flags: this sweep's, the next one's (cleared now), and the previous
+    // one's, which a block that just left the last barrier may still be reading
+    int* ch = changed + it % 3;
+    if (t == 0) changed[(it + 1) % 3] = 0;
+    for (i64 e = t; e < E; e += T) {
+      kill[ev[e].x] = INT32_MAX;
+      kill[ev[e].y] = INT32_MAX;
+    }
+    grid_sync(bar, nb);
+    for (i64 e = t; e < E; e += T)
+      if (fired[e]) atomicMin(&kill[ev[e].x], (i32)e);
+    grid_sync(bar, nb);
+    bool mine = false;
+    for (i64 e = t; e < E; e += T) {
+      const uint8_t f = (kill[ev[e].x] >= (i32)e && kill[ev[e].y] >= (i32)e) ? 1 : 0;
+      if (f != fired[e]) {
+        fired[e] = f;
+        mine = true;
+      }
+    }
+    if (__syncthreads_or(mine) && threadIdx.x == 0) atomicExch(ch, 1);
+    grid_sync(bar, nb);
+    if (!*(volatile int*)ch) break;
+  }
+  unsigned long long n = 0;
+  for (i64 e = t; e < E; e += T)
+    if (fired[e]) {
+      colors[ev[e].x] = 0;
+      n++;
+    }
+  n = __reduce_add_sync(0xffffffffu, (unsigned)n);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(conflicts, n);
+}
+
 // Incremental detection: an event (equal non-zero colours on a scanned pair) can
 // only exist if one endpoint changed colour since the previous detection (which
 // left no conflicting pair behind, and unchanged pairs keep their colours).  Mark
@@ -520,7 +582,21 @@ void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
   mark_t();
   S.fired.reserve(E, s);
   S.kill.reserve(num_vertices, s);
-  k_resolve<<<1, 1024, 0, s>>>(S.ev.p, E, S.fired.p, S.kill.p, A.colors, conflicts_dev, A.sequential);
+  if (A.sequential && E > 32768) {
+    S.result.reserve(4, s);
+    CUDA_CHECK(cudaMemsetAsync(S.result.p, 0, 4 * sizeof(unsigned long long), s));
+    unsigned* bar = reinterpret_cast<unsigned*>(S.result.p);
+    int* changed = reinterpret_cast<int*>(S.result.p + 1);
+    const int2* evp = S.ev.p;
+    uint8_t* fp = S.fired.p;
+    i32* kp = S.kill.p;
+    i32* cp = A.colors;
+    void* args[] = {(void*)&evp, (void*)&E, (void*)&fp, (void*)&kp, (void*)&cp, (void*)&conflicts_dev, (void*)&bar,
+                    (void*)&changed};
+    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_resolve_grid, dim3(num_sms()), dim3(1024), args, 0, s));
+  } else {
+    k_resolve<<<1, 1024, 0, s>>>(S.ev.p, E, S.fired.p, S.kill.p, A.colors, conflicts_dev, A.sequential);
+  }
   count_launch();
   CUDA_CHECK(cudaGetLastError());
   mark_t();
