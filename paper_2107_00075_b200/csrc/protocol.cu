@@ -143,7 +143,7 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     i64 cnt[6];
     CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 3 * sizeof(i64), cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-    if (dist == 1 && cnt[1] == 0 && !always_spec) {  // no heavy rows
+    if (dist == 1 && cnt[1] == 0 && !always_spec && !S.keep_free) {  // no heavy rows
       algo = CHROMA_ALGO_GAUSS_SEIDEL;
       goto gauss_seidel;
     }
@@ -366,7 +366,16 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   // round-0 schedule: 0 auto (levels if the DAG is wide, else rank-interleaved for
   // virtual ranks, else id order), 1 levels only, 2 interleave only, 3 id order
   static const int sched = (int)env_i64("CHROMA_GS_SCHEDULE", 0);
+  // Level frontiers expand row by row: hub rows (R-MAT) make a level step as slow as
+  // its longest row and such DAGs are deep anyway, and the free mode only takes the
+  // ordered kernel on hub-free worklists -- levels are built for bounded-degree graphs.
+  static const i64 level_max_deg = env_i64("CHROMA_LEVEL_MAX_DEG", 1024);
   const bool fast = algo == CHROMA_ALGO_FREE && !no_fast && (!w.connected || w.p2p || w.P == 1);
+  // free-running D1 over several ranks: colour the hubs of all ranks first (hubs.cu)
+  static const bool no_hubs = std::getenv("CHROMA_NO_HUBS") != nullptr;
+  const i64 hub_deg = env_i64("CHROMA_HUB_DEG", 4096);  // read per call (tests vary it)
+  const bool hubs_first = algo == CHROMA_ALGO_FREE && !d2 && w.P > 1 && !no_hubs &&
+                          (w.all_local() || w.connected) && w.delta_max > hub_deg;
   if (fast) {
     halo_route_index(w);
     w.next_wl.reserve(w.NL + 1, s);
@@ -398,6 +407,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   da.owned_flag = w.owned_flag.p;
   w.det.prev_valid = false;
   const bool remote = w.connected && w.P > 1;
+  bool hubs_done = false;
   for (;;) {
     if (round > max_rounds) {
       status = CHROMA_ENONCONV;
@@ -409,6 +419,14 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     }
     CUDA_CHECK(cudaMemsetAsync(w.stats.p, 0, sizeof(unsigned long long) * (nstats + 1), s));
     CUDA_CHECK(cudaEventRecord(ev[0], s));
+    if (round == 0 && hubs_first) {
+      // hubs.cu: every rank's hubs coloured once, identically everywhere; the
+      // round-0 worklist below then holds the light vertices only, and every round
+      // keeps the speculative path (the ordered kernel's id chain is long on such
+      // graphs even without the hubs)
+      hubs_done = hub_precolor(w, (i32)hub_deg) > 0;
+    }
+    w.cs.keep_free = hubs_done;
     if (fast && round > 0) {
       // the previous detection's owned losers, ascending
       nwl_host = (i64)hs[(size_t)nstats];
@@ -440,7 +458,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         }
         i64 n = 0;
         // levels when the DAG is wide; else (virtual ranks) rank-interleaved id order
-        w.level_mode = (sched == 0 || sched == 1) &&
+        w.level_mode = (sched == 0 || sched == 1) && w.delta_max <= level_max_deg &&
                        build_level_order(w.g.rowptr.p, w.g.col.p, w.NL, w.cs.wl.p, owned, w.level_wl, n, s);
         w.level_n = w.level_mode ? n : 0;
         if (!w.level_mode && (sched == 0 || sched == 2) &&
@@ -458,6 +476,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, nwl_host, true, dist, partial,
               algo, true, w.cs, s, gs_like ? ev[6] : nullptr, gs_like ? ev[7] : nullptr);
     w.cs.level_wl = nullptr;
+    w.cs.keep_free = false;
     CUDA_CHECK(cudaEventRecord(ev[1], s));
     // exchange: every ghost takes its owner's colour; accounting is changed-only
     const bool listed = fast && round > 0;  // exchange and detection driven by lists

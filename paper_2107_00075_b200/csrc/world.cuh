@@ -39,8 +39,24 @@ struct ColorScratch {
   const i32* level_wl = nullptr;
   i64 level_n = 0;
   bool level_mode = true;
+  // free mode: keep the speculative path even without heavy rows (hubs pre-coloured)
+  bool keep_free = false;
   DBuf<i64> level_n_dev;
   DBuf<i64> fcnt;
+  FreeWaveScratch fw;
+};
+
+// Global hub pre-colouring scratch (hubs.cu)
+struct HubScratch {
+  DBuf<uint8_t> flags;
+  DBuf<i32> lhubs;
+  DBuf<i64> nlh, lcnt, loff, lgid, lnbr;   // this world's owned hubs
+  DBuf<i64> ggid, gcnt, gnbr;              // all-gathered (connected worlds)
+  DBuf<i64> rowptr, cntz;
+  DBuf<u64> keys;                          // sorted (gid << 32 | H index)
+  DBuf<i32> col, colors, list, ovf;
+  DBuf<i64> novf;
+  DBuf<unsigned long long> missing;
   FreeWaveScratch fw;
 };
 
@@ -102,6 +118,7 @@ struct World {
   // protocol scratch
   ColorScratch cs;
   DetectScratch det;
+  HubScratch hub;
   DBuf<unsigned long long> stats;  // [0] conflicts [1] bytes [2] msgs [3..3+P) recolored
   DBuf<i32> deg_override;
   // schedule of the full owned worklist (computed on first use, -1 = not yet)
@@ -147,6 +164,11 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
 // vertices per rank, contiguous in wl).  gs_levels.cu.
 bool build_rank_interleave(const i32* wl, const std::vector<i64>& rank_counts, DBuf<i32>& out, i64& nout,
                            cudaStream_t s);
+
+// Colour every hub (global degree > T) of all ranks exactly, identically on every
+// rank, into the owned hubs and the ghost copies of hubs; returns the number of hubs.
+// Collective over the processes of a connected world.  hubs.cu.
+i64 hub_precolor(World& w, i32 T);
 
 // Colour the worklist of a CSR (absolute vertex ids).  `wl_sorted_unique` skips the
 // device sort/dedupe for protocol worklists that are produced in order.

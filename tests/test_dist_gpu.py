@@ -42,14 +42,19 @@ def test_dist_parity_nccl(n):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("n,p2p", [(2, True), (4, True), (2, False)])
-def test_dist_free_running(n, p2p):
-    """Free-running mode across processes: NVLink peer-memory halo (or NCCL only)."""
+@pytest.mark.parametrize("n,p2p,hub_deg", [(2, True, None), (4, True, None), (2, False, None),
+                                           (2, True, 48), (4, True, 48), (2, False, 48)])
+def test_dist_free_running(n, p2p, hub_deg):
+    """Free-running mode across processes: NVLink peer-memory halo (or NCCL only);
+    hub_deg lowers the global hub pre-colouring threshold (hubs.cu) so the small test
+    graphs take that path too."""
     if _ngpu() < n:
         pytest.skip(f"needs {n} GPUs")
     env = dict(os.environ)
     if not p2p:
         env["CHROMA_NO_P2P"] = "1"
+    if hub_deg is not None:
+        env["CHROMA_HUB_DEG"] = str(hub_deg)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "dist_free_main.py")]

@@ -85,6 +85,21 @@ def test_free_rmat_heavy_waves_recolor_degrees():
     assert colors.max() <= 1.05 * ref.max() + 1
 
 
+@pytest.mark.parametrize("P", [2, 8])
+@pytest.mark.parametrize("mode", ["d1", "d1-2gl"])
+def test_free_rmat_hubs_first(P, mode, monkeypatch):
+    """Global hub pre-colouring (hubs.cu) with a low threshold, so a small R-MAT has
+    hundreds of hubs spread over the ranks: proper, converged, and close to the
+    oracle's count."""
+    monkeypatch.setenv("CHROMA_HUB_DEG", "48")
+    g = G.gen_rmat(14, 16, 1)
+    assert int(np.diff(g.row_offsets).max()) > 48
+    colors, ref, reports = _run(g, mode, P)
+    _check_proper(g, colors, mode)
+    assert reports[-1].conflicts == 0
+    assert colors.max() <= 1.10 * ref.max() + 1, (colors.max(), ref.max())
+
+
 @pytest.mark.parametrize("mode,builder", [
     ("d2", lambda: G.gen_hex_mesh(24, 24, 24)),
     ("pd2", lambda: G.gen_random_bipartite(1 << 12, 16, 5).graph),
