@@ -43,7 +43,19 @@ __device__ __forceinline__ void for_each_in_set(const i64* rowptr, const i32* co
                                                 F&& f) {
   const i64 rs = rowptr[v], re = rowptr[v + 1];
   if (DIST == 1) {
-    for (i64 e = rs + t; e < re; e += stride) f(col[e]);
+    // 4 column entries per thread in flight; the callback's gathers follow them
+    constexpr int U = 4;
+    for (i64 e0 = rs + t; e0 < re; e0 += (i64)U * stride) {
+      i32 x[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const i64 e = e0 + (i64)u * stride;
+        x[u] = e < re ? ld_stream(col + e) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (x[u] >= 0) f(x[u]);
+    }
   } else if (stride == 32) {
     for (i64 e = rs; e < re; e++) {
       const i32 u = col[e];
@@ -121,7 +133,7 @@ __global__ void k_color_light(const i64* rowptr, const i32* col, i32* colors, co
       a.clear();
       const bool count = skip < 0;
       for_each_in_set<DIST, PARTIAL>(rowptr, col, v, t, G, [&](i32 x) {
-        a.add(x, v, ld_relaxed(colors + x), base, snapshot && count);
+        a.add(x, v, ld_relaxed_nb(colors + x), base, snapshot && count);
       });
       if (count) skip = snapshot ? min((int)__reduce_add_sync(gmask, (unsigned)a.rank), rank_cap) : 0;
       u32 mw[WORDS];
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_color_heavy(const i64* rowptr
       a.clear();
       const bool count = skip < 0;
       for_each_in_set<DIST, PARTIAL>(rowptr, col, v, t, HEAVY_THREADS, [&](i32 x) {
-        a.add(x, v, ld_relaxed(colors + x), base, snapshot && count);
+        a.add(x, v, ld_relaxed_nb(colors + x), base, snapshot && count);
       });
 #pragma unroll
       for (int w = 0; w < WORDS; w++) {
@@ -187,6 +199,65 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_color_heavy(const i64* rowptr
   }
 }
 
+// Tiny rows (distance 1, degree <= 63): one thread per vertex.  First fit of a row of
+// d entries is at most d + 1 <= 64, so one 64-bit mask covers it (no window loop,
+// no lane reductions); column entries and colours are gathered in batches of 8 so
+// a thread keeps 8 independent loads in flight.  Isolated vertices take colour 1.
+constexpr int TB = 8;
+__global__ void k_color_tiny(const i64* rowptr, const i32* col, i32* colors, const i32* list, const i64* n_dev) {
+  const i64 n = *n_dev;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = list[i];
+    const i64 rs = rowptr[v], re = rowptr[v + 1];
+    u64 m = 0;
+    for (i64 e0 = rs; e0 < re; e0 += TB) {
+      i32 x[TB], c[TB];
+#pragma unroll
+      for (int u = 0; u < TB; u++) x[u] = e0 + u < re ? ld_stream(col + e0 + u) : -1;
+#pragma unroll
+      for (int u = 0; u < TB; u++) c[u] = x[u] >= 0 ? ld_relaxed_nb(colors + x[u]) : 0;
+#pragma unroll
+      for (int u = 0; u < TB; u++) {
+        const i32 a = iabs(c[u]);
+        if (a >= 1 && a <= 64) m |= 1ull << (a - 1);
+      }
+    }
+    st_relaxed(colors + v, -__ffsll((long long)~m));
+  }
+}
+
+__global__ void k_losers_tiny(const i64* rowptr, const i32* col, i32* colors, const i32* list, const i64* n_dev,
+                              i32* next, unsigned long long* nnext) {
+  const int lane = threadIdx.x & 31;
+  const i64 n = *n_dev;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 b = (blockIdx.x * (i64)blockDim.x + threadIdx.x) & ~31ll; b < n; b += stride) {
+    const i64 i = b + lane;
+    bool lose = false;
+    i32 v = 0;
+    if (i < n) {
+      v = list[i];
+      const i32 c = iabs(ld_relaxed_nb(colors + v));
+      const i64 rs = rowptr[v], re = rowptr[v + 1];
+      for (i64 e0 = rs; e0 < re && !lose; e0 += TB) {
+        i32 x[TB], cx[TB];
+#pragma unroll
+        for (int u = 0; u < TB; u++) x[u] = e0 + u < re ? ld_stream(col + e0 + u) : -1;
+#pragma unroll
+        for (int u = 0; u < TB; u++) cx[u] = x[u] > v ? ld_relaxed_nb(colors + x[u]) : 0;
+#pragma unroll
+        for (int u = 0; u < TB; u++) lose |= x[u] > v && iabs(cx[u]) == c;
+      }
+      st_relaxed(colors + v, lose ? 0 : c);
+    }
+    const u32 m = __ballot_sync(FULL, lose);
+    unsigned long long o = 0;
+    if (lane == 0 && m) o = atomicAdd(nnext, (unsigned long long)__popc(m));
+    o = __shfl_sync(FULL, o, 0);
+    if (lose) next[o + __popc(m & ((1u << lane) - 1))] = v;
+  }
+}
+
 // Resolution: v keeps its colour unless a larger-id member of its set has it.
 // G lanes per vertex as above; losers are a small fraction, one atomic each.
 template <int DIST, bool PARTIAL, int G>
@@ -202,7 +273,7 @@ __global__ void k_losers_light(const i64* rowptr, const i32* col, i32* colors, c
     const i32 c = iabs(ld_relaxed(colors + v));
     bool hit = false;
     for_each_in_set<DIST, PARTIAL>(rowptr, col, v, t, G, [&](i32 x) {
-      if (x > v && iabs(ld_relaxed(colors + x)) == c) hit = true;
+      if (x > v && iabs(ld_relaxed_nb(colors + x)) == c) hit = true;
     });
     const bool any = __any_sync(gmask, hit);
     if (t == 0) {
@@ -226,7 +297,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_losers_heavy(const i64* rowpt
     const i32 c = iabs(ld_relaxed(colors + v));
     bool hit = false;
     for_each_in_set<DIST, PARTIAL>(rowptr, col, v, t, HEAVY_THREADS, [&](i32 x) {
-      if (x > v && iabs(ld_relaxed(colors + x)) == c) hit = true;
+      if (x > v && iabs(ld_relaxed_nb(colors + x)) == c) hit = true;
     });
     if (__any_sync(FULL, hit) && (t & 31) == 0) shit = 1;
     __syncthreads();
@@ -238,28 +309,60 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_losers_heavy(const i64* rowpt
   }
 }
 
-// worklist -> tiny / light / heavy lists by row length (warp-aggregated appends)
-__global__ void k_split(const i32* wl, const i64* n_dev, const i64* rowptr, i64 tiny_deg, i64 heavy_deg, i32* tiny,
-                        i32* light, i32* heavy, unsigned long long* cnt /* [light, heavy, tiny] */) {
-  const int lane = threadIdx.x & 31;
+// worklist -> tiny / light / heavy lists by row length.  Each 256-thread block takes
+// tiles of 256 x SPI entries; per-warp ballots are combined in shared memory so a
+// tile costs one global atomic per class (appends are unordered).
+constexpr int SPI = 8;
+__global__ void __launch_bounds__(256) k_split(const i32* wl, const i64* n_dev, const i64* rowptr, i64 tiny_deg,
+                                               i64 heavy_deg, i32* tiny, i32* light, i32* heavy,
+                                               unsigned long long* cnt /* [light, heavy, tiny] */) {
+  __shared__ u32 wtot[3][8];
+  __shared__ unsigned long long base[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 below = (1u << lane) - 1;
   const i64 n = *n_dev;
-  const i64 stride = (i64)gridDim.x * blockDim.x;
-  for (i64 b = (blockIdx.x * (i64)blockDim.x + threadIdx.x) & ~31ll; b < n; b += stride) {
-    const i64 i = b + lane;
-    const bool valid = i < n;
-    const i32 v = valid ? wl[i] : 0;
-    const i64 d = valid ? rowptr[v + 1] - rowptr[v] : 0;
-    const int cls = !valid ? -1 : d > heavy_deg ? 1 : d <= tiny_deg ? 2 : 0;
-    const u32 below = (1u << lane) - 1;
-    i32* out[3] = {light, heavy, tiny};
+  constexpr i64 TILE = 256 * SPI;
+  i32* out[3] = {light, heavy, tiny};
+  for (i64 t0 = (i64)blockIdx.x * TILE; t0 < n; t0 += (i64)gridDim.x * TILE) {
+    i32 v[SPI];
+    int cls[SPI];
+    u32 run[3] = {0, 0, 0};
 #pragma unroll
-    for (int k = 0; k < 3; k++) {
-      const u32 m = __ballot_sync(FULL, cls == k);
-      unsigned long long o = 0;
-      if (lane == 0 && m) o = atomicAdd(cnt + k, (unsigned long long)__popc(m));
-      o = __shfl_sync(FULL, o, 0);
-      if (cls == k) out[k][o + __popc(m & below)] = v;
+    for (int k = 0; k < SPI; k++) {
+      const i64 i = t0 + (i64)k * 256 + threadIdx.x;
+      v[k] = i < n ? wl[i] : -1;
     }
+#pragma unroll
+    for (int k = 0; k < SPI; k++) {
+      const i64 d = v[k] >= 0 ? rowptr[v[k] + 1] - rowptr[v[k]] : 0;
+      cls[k] = v[k] < 0 ? -1 : d > heavy_deg ? 1 : d <= tiny_deg ? 2 : 0;
+#pragma unroll
+      for (int c = 0; c < 3; c++) run[c] += __popc(__ballot_sync(FULL, cls[k] == c));
+    }
+    if (lane < 3) wtot[lane][warp] = run[lane];
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      u32 tot = 0;
+      for (int w = 0; w < 8; w++) tot += wtot[threadIdx.x][w];
+      base[threadIdx.x] = tot ? atomicAdd(cnt + threadIdx.x, (unsigned long long)tot) : 0;
+    }
+    __syncthreads();
+    unsigned long long o[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      o[c] = base[c];
+      for (int w = 0; w < warp; w++) o[c] += wtot[c][w];
+    }
+#pragma unroll
+    for (int k = 0; k < SPI; k++) {
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        const u32 m = __ballot_sync(FULL, cls[k] == c);
+        if (cls[k] == c) out[c][o[c] + __popc(m & below)] = v[k];
+        o[c] += __popc(m);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -497,7 +600,7 @@ void launch_free_split(const i32* wl, const i64* n_dev, i64 n_max, const i64* ro
                        FreeLists& f, int p, cudaStream_t s) {
   CUDA_CHECK(cudaMemsetAsync(f.cnt + 3 * p, 0, 3 * sizeof(i64), s));
   if (n_max <= 0) return;
-  k_split<<<grid_for(n_max, 256, num_sms() * 8), 256, 0, s>>>(
+  k_split<<<grid_for(n_max, 256 * SPI, num_sms() * 8), 256, 0, s>>>(
       wl, n_dev, rowptr, tiny_deg, heavy_deg, f.tiny[p], f.light[p], f.heavy[p],
       reinterpret_cast<unsigned long long*>(f.cnt + 3 * p));
   count_launch();
@@ -519,15 +622,26 @@ void launch_free_iteration(const i64* rowptr, const i32* col, i32* colors, FreeL
     FREE_DISPATCH(k_color_heavy, gh, HEAVY_THREADS, rowptr, col, colors, f.heavy[p], cnt + 1, snapshot, rank_cap);
   if (nlight_max > 0)
     FREE_DISPATCH_G(k_color_light, 32, gl, 256, rowptr, col, colors, f.light[p], cnt + 0, snapshot, rank_cap);
-  if (ntiny_max > 0)
+  // tiny rows exist for distance 1 only (launch_free_split); thread per vertex
+  const bool tiny_thread = dist == 1 && !snapshot;
+  const int gtt = grid_for(std::max<i64>(ntiny_max, 1), 256, num_sms() * 16);
+  if (ntiny_max > 0 && tiny_thread) {
+    k_color_tiny<<<gtt, 256, 0, s>>>(rowptr, col, colors, f.tiny[p], cnt + 2);
+    count_launch();
+  } else if (ntiny_max > 0) {
     FREE_DISPATCH_G(k_color_light, 8, gt, 256, rowptr, col, colors, f.tiny[p], cnt + 2, snapshot, rank_cap);
+  }
   if (nheavy_max > 0)
     FREE_DISPATCH(k_losers_heavy, gh, HEAVY_THREADS, rowptr, col, colors, f.heavy[p], cnt + 1, f.heavy[q],
                   next_cnt + 1);
   if (nlight_max > 0)
     FREE_DISPATCH_G(k_losers_light, 32, gl, 256, rowptr, col, colors, f.light[p], cnt + 0, f.light[q], next_cnt + 0);
-  if (ntiny_max > 0)
+  if (ntiny_max > 0 && tiny_thread) {
+    k_losers_tiny<<<gtt, 256, 0, s>>>(rowptr, col, colors, f.tiny[p], cnt + 2, f.tiny[q], next_cnt + 2);
+    count_launch();
+  } else if (ntiny_max > 0) {
     FREE_DISPATCH_G(k_losers_light, 8, gt, 256, rowptr, col, colors, f.tiny[p], cnt + 2, f.tiny[q], next_cnt + 2);
+  }
 }
 
 }  // namespace chroma

@@ -124,6 +124,15 @@ __device__ __forceinline__ i32 ld_relaxed(const i32* p) {
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// same load without the compiler memory barrier: independent loads around it may be
+// batched (speculative gathers, where the value is only a hint until resolution)
+__device__ __forceinline__ i32 ld_relaxed_nb(const i32* p) {
+  i32 v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+// streaming (evict-first) load of a CSR column entry: keeps the gathered colours in L2
+__device__ __forceinline__ i32 ld_stream(const i32* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_relaxed(i32* p, i32 v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

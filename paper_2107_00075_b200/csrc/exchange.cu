@@ -10,18 +10,35 @@
 namespace chroma {
 namespace {
 
+// Per-(src, dst) counters are accumulated in shared memory (one global atomic per
+// block and pair at the end): global atomics per entry on a handful of addresses
+// serialise the whole kernel.
+constexpr int SHARED_PAIRS = 4096;
+
 __global__ void k_exchange(const i32* routed, i64 nrouted, const i64* st_off, const i32* st_dst,
                            const i32* st_pair, i32* colors, i32* last_sent, bool changed_only,
-                           bool write_all, unsigned long long* pair_cnt) {
+                           bool write_all, unsigned long long* pair_cnt, i64 npairs) {
+  __shared__ unsigned sc[SHARED_PAIRS];
+  const bool local = npairs <= SHARED_PAIRS;
+  if (local)
+    for (i64 k = threadIdx.x; k < npairs; k += blockDim.x) sc[k] = 0;
+  __syncthreads();
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nrouted; i += (i64)gridDim.x * blockDim.x) {
     const i32 c = colors[routed[i]];
     const bool send = !changed_only || last_sent[i] != c;
     if (send) last_sent[i] = c;
     for (i64 t = st_off[i]; t < st_off[i + 1]; t++) {
       if (send || write_all) colors[st_dst[t]] = c;
-      if (send) atomicAdd(&pair_cnt[st_pair[t]], 1ull);
+      if (send) {
+        if (local) atomicAdd(&sc[st_pair[t]], 1u);
+        else atomicAdd(&pair_cnt[st_pair[t]], 1ull);
+      }
     }
   }
+  __syncthreads();
+  if (local)
+    for (i64 k = threadIdx.x; k < npairs; k += blockDim.x)
+      if (sc[k]) atomicAdd(&pair_cnt[k], (unsigned long long)sc[k]);
 }
 
 // stats2[0] += 12 * pairs sent, stats2[1] += non-empty inboxes; clears pair_cnt
@@ -49,10 +66,10 @@ __global__ void k_pair_stats(unsigned long long* pair_cnt, i64 npairs, unsigned 
 
 void launch_exchange_local(const i32* routed, i64 nrouted, const i64* st_off, const i32* st_dst,
                            const i32* st_pair, i32* colors, i32* last_sent, bool changed_only,
-                           bool write_all, unsigned long long* pair_cnt, cudaStream_t s) {
+                           bool write_all, unsigned long long* pair_cnt, i64 npairs, cudaStream_t s) {
   if (nrouted <= 0) return;
   k_exchange<<<grid_for(nrouted, 256, num_sms() * 16), 256, 0, s>>>(
-      routed, nrouted, st_off, st_dst, st_pair, colors, last_sent, changed_only, write_all, pair_cnt);
+      routed, nrouted, st_off, st_dst, st_pair, colors, last_sent, changed_only, write_all, pair_cnt, npairs);
   count_launch();
   CUDA_CHECK(cudaGetLastError());
 }

@@ -28,10 +28,18 @@ __global__ void k_route_index(const i32* routed, i64 n, i32* idx) {
     idx[routed[i]] = (i32)i;
 }
 
+// (src, dst) message counters: shared per block, flushed with one atomic per pair
+constexpr int PAIR_SHARED = 4096;
+
 // virtual ranks: worklist vertex -> its ghost copies (same array) + changed flags
 __global__ void k_xchg_local_list(const i32* wl, const i64* nwl_dev, const i32* route_idx, const i64* st_off,
                                   const i32* st_dst, const i32* st_pair, i32* colors, i32* last_sent,
-                                  unsigned long long* pair_cnt) {
+                                  unsigned long long* pair_cnt, i64 npairs) {
+  __shared__ unsigned sc[PAIR_SHARED];
+  const bool local = npairs <= PAIR_SHARED;
+  if (local)
+    for (i64 k = threadIdx.x; k < npairs; k += blockDim.x) sc[k] = 0;
+  __syncthreads();
   const i64 n = *nwl_dev;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 v = wl[i];
@@ -43,15 +51,27 @@ __global__ void k_xchg_local_list(const i32* wl, const i64* nwl_dev, const i32* 
     for (i64 t = st_off[r]; t < st_off[r + 1]; t++) {
       const i32 d = st_dst[t];
       colors[d] = c;
-      if (send) atomicAdd(&pair_cnt[st_pair[t]], 1ull);
+      if (send) {
+        if (local) atomicAdd(&sc[st_pair[t]], 1u);
+        else atomicAdd(&pair_cnt[st_pair[t]], 1ull);
+      }
     }
   }
+  __syncthreads();
+  if (local)
+    for (i64 k = threadIdx.x; k < npairs; k += blockDim.x)
+      if (sc[k]) atomicAdd(&pair_cnt[k], (unsigned long long)sc[k]);
 }
 
 // one rank per process: worklist vertex -> peers' ghost slots over NVLink
 __global__ void k_xchg_p2p(const i32* wl, const i64* nwl_dev, i64 lid_off, const i64* rs_off, const i32* rs_peer,
                            const i32* rs_rlid, i32* rs_last, const i32* colors, i32* const* peer_colors,
-                           unsigned long long* pair_cnt) {
+                           unsigned long long* pair_cnt, i32 P) {
+  __shared__ unsigned sc[PAIR_SHARED];
+  const bool local = P <= PAIR_SHARED;
+  if (local)
+    for (int k = threadIdx.x; k < P; k += blockDim.x) sc[k] = 0;
+  __syncthreads();
   const i64 n = *nwl_dev;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 v = wl[i];
@@ -61,12 +81,17 @@ __global__ void k_xchg_p2p(const i32* wl, const i64* nwl_dev, i64 lid_off, const
       const i32 p = rs_peer[e], r = rs_rlid[e];
       if (rs_last[e] != c) {
         rs_last[e] = c;
-        atomicAdd(&pair_cnt[p], 1ull);
+        if (local) atomicAdd(&sc[p], 1u);
+        else atomicAdd(&pair_cnt[p], 1ull);
       }
       peer_colors[p][r] = c;
     }
   }
   __threadfence_system();
+  __syncthreads();
+  if (local)
+    for (int k = threadIdx.x; k < P; k += blockDim.x)
+      if (sc[k]) atomicAdd(&pair_cnt[k], (unsigned long long)sc[k]);
 }
 
 // owned losers of the detection -> colour 0 in every ghost copy (virtual ranks)
@@ -190,7 +215,7 @@ void halo_barrier(World& w) {
 void halo_exchange_local_list(World& w, const i32* wl, const i64* nwl_dev, i64 nwl_max) {
   if (w.nrouted == 0 || nwl_max <= 0) return;
   k_xchg_local_list<<<G(nwl_max), 256, 0, w.stream>>>(wl, nwl_dev, w.route_idx.p, w.st_off.p, w.st_dst.p,
-                                                       w.st_pair.p, w.colors.p, w.last_sent.p, w.pair_cnt.p);
+                                                       w.st_pair.p, w.colors.p, w.last_sent.p, w.pair_cnt.p, (i64)w.P * w.P);
   count_launch();
   CUDA_CHECK(cudaGetLastError());
 }
@@ -199,7 +224,7 @@ void halo_exchange_p2p(World& w, const i32* wl, const i64* nwl_dev, i64 nwl_max)
   cudaStream_t s = w.stream;
   if (nwl_max > 0 && w.nsend > 0) {
     k_xchg_p2p<<<G(nwl_max), 256, 0, s>>>(wl, nwl_dev, w.ranks[0].lid_off, w.rs_off.p, w.rs_peer.p, w.rs_rlid.p,
-                                          w.rs_last.p, w.colors.p, w.peer_colors.p, w.pair_cnt.p);
+                                          w.rs_last.p, w.colors.p, w.peer_colors.p, w.pair_cnt.p, w.P);
     count_launch();
   }
   CUDA_CHECK(cudaGetLastError());

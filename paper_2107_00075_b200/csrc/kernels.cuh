@@ -149,7 +149,7 @@ void run_detect(const DetectArgs& a, i64 num_vertices, DetectScratch& S,
 // ---------------------------------------------------------------- exchange (device copy)
 void launch_exchange_local(const i32* routed, i64 nrouted, const i64* st_off, const i32* st_dst,
                            const i32* st_pair, i32* colors, i32* last_sent, bool changed_only,
-                           bool write_all, unsigned long long* pair_cnt, cudaStream_t s);
+                           bool write_all, unsigned long long* pair_cnt, i64 npairs, cudaStream_t s);
 void launch_pair_stats(unsigned long long* pair_cnt, i64 npairs, unsigned long long* stats2,
                        cudaStream_t s);
 

@@ -167,15 +167,20 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
                      std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw0).count(),
                      (long long)cnt[0]);
     }
+    auto tl = std::chrono::steady_clock::now();
     for (int it = 0; it < MAX_SWEEPS; it++) {
       const int p = it & 1, q = p ^ 1;
       launch_free_iteration(rowptr, col, cur, f, p, cnt + 3 * p, it > 0 ? (int)rank_cap : 0, dist, partial, s);
       CUDA_CHECK(cudaMemcpyAsync(cnt + 3 * q, S.fcnt.p + 3 * q, 3 * sizeof(i64), cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
-      if (trace)
-        std::fprintf(stderr, "[free] it=%d light %lld -> %lld heavy %lld -> %lld tiny %lld -> %lld\n", it,
+      if (trace) {
+        const auto tn = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[free] it=%d light %lld -> %lld heavy %lld -> %lld tiny %lld -> %lld (%.0f us)\n", it,
                      (long long)cnt[3 * p], (long long)cnt[3 * q], (long long)cnt[3 * p + 1],
-                     (long long)cnt[3 * q + 1], (long long)cnt[3 * p + 2], (long long)cnt[3 * q + 2]);
+                     (long long)cnt[3 * q + 1], (long long)cnt[3 * p + 2], (long long)cnt[3 * q + 2],
+                     std::chrono::duration<double, std::micro>(tn - tl).count());
+        tl = tn;
+      }
       const i64 pend = cnt[3 * q] + cnt[3 * q + 1] + cnt[3 * q + 2];
       if (pend > 0 && it + 1 >= tail_after && pend <= tail_n && !no_waves) {
         // a small remainder that keeps colliding is a dense cluster: finish it
@@ -283,13 +288,42 @@ __global__ void k_changed(const i32* routed, i64 n, const i32* colors, i32* last
     changed[v] = send ? 1 : 0;
   }
 }
+// send lists are grouped by peer: a thread's run of one peer is counted in a
+// register and flushed into a shared counter when the peer changes, one global
+// atomic per block and peer at the end
 __global__ void k_pack(const i32* send_lids, const i32* send_peer, i64 n, const i32* colors,
-                       const uint8_t* changed, i32* buf, unsigned long long* peer_cnt) {
+                       const uint8_t* changed, i32* buf, unsigned long long* peer_cnt, i32 P) {
+  __shared__ unsigned sc[1024];
+  const bool local = P <= 1024;
+  if (local)
+    for (int k = threadIdx.x; k < P; k += blockDim.x) sc[k] = 0;
+  __syncthreads();
+  i32 cur = -1;
+  unsigned run = 0;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 v = send_lids[i];
     buf[i] = colors[v];
-    if (changed[v]) atomicAdd(&peer_cnt[send_peer[i]], 1ull);
+    if (changed[v]) {
+      const i32 p = send_peer[i];
+      if (p != cur) {
+        if (run) {
+          if (local) atomicAdd(&sc[cur], run);
+          else atomicAdd(&peer_cnt[cur], (unsigned long long)run);
+        }
+        cur = p;
+        run = 0;
+      }
+      run++;
+    }
   }
+  if (run) {
+    if (local) atomicAdd(&sc[cur], run);
+    else atomicAdd(&peer_cnt[cur], (unsigned long long)run);
+  }
+  __syncthreads();
+  if (local)
+    for (int k = threadIdx.x; k < P; k += blockDim.x)
+      if (sc[k]) atomicAdd(&peer_cnt[k], (unsigned long long)sc[k]);
 }
 __global__ void k_unpack(const i32* recv_lids, i64 n, const i32* buf, i32* colors) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
@@ -315,7 +349,7 @@ static void exchange_remote(World& w, bool changed_only) {
                                                    w.last_sent_remote.p, changed_only, w.changed.p);
   if (w.nsend)
     k_pack<<<G(w.nsend), 256, 0, s>>>(w.send_lids.p, w.send_peer.p, w.nsend, w.colors.p, w.changed.p,
-                                       w.sendbuf.p, w.pair_cnt.p);
+                                       w.sendbuf.p, w.pair_cnt.p, w.P);
   count_launch(2);
   NCCL_CHECK(ncclGroupStart());
   for (i32 p = 0; p < w.P; p++) {
@@ -408,6 +442,17 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   w.det.prev_valid = false;
   const bool remote = w.connected && w.P > 1;
   bool hubs_done = false;
+  // CHROMA_ROUND_TRACE: synchronised per-phase host timings of round 0 (dev aid)
+  static const bool round_trace = std::getenv("CHROMA_ROUND_TRACE") != nullptr;
+  auto rt_last = std::chrono::steady_clock::now();
+  i64 rt_round = 0;
+  auto rt_mark = [&](const char* what) {
+    if (!round_trace || rt_round != 0) return;
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    const auto tn = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[round0] %-18s %8.1f us\n", what, std::chrono::duration<double, std::micro>(tn - rt_last).count());
+    rt_last = tn;
+  };
   for (;;) {
     if (round > max_rounds) {
       status = CHROMA_ENONCONV;
@@ -419,6 +464,8 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     }
     CUDA_CHECK(cudaMemsetAsync(w.stats.p, 0, sizeof(unsigned long long) * (nstats + 1), s));
     CUDA_CHECK(cudaEventRecord(ev[0], s));
+    rt_round = round;
+    rt_mark("start");
     if (round == 0 && hubs_first) {
       // hubs.cu: every rank's hubs coloured once, identically everywhere; the
       // round-0 worklist below then holds the light vertices only, and every round
@@ -473,8 +520,10 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         w.cs.level_mode = w.level_mode;
       }
     }
+    rt_mark("hubs+worklist");
     color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, nwl_host, true, dist, partial,
               algo, true, w.cs, s, gs_like ? ev[6] : nullptr, gs_like ? ev[7] : nullptr);
+    rt_mark("color");
     w.cs.level_wl = nullptr;
     w.cs.keep_free = false;
     CUDA_CHECK(cudaEventRecord(ev[1], s));
@@ -490,8 +539,11 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         halo_exchange_p2p(w, w.cs.wl.p, w.cs.nwl.p, nwl_host);
         launch_pair_stats(w.pair_cnt.p, w.P, w.stats.p + 1, s);
       } else {
+        rt_mark("pre-exchange");
         exchange_remote(w, round > 0);
+        rt_mark("exchange_remote");
         if (fast) halo_init_p2p_last(w);
+        rt_mark("init_p2p_last");
       }
     }
     CUDA_CHECK(cudaEventRecord(ev[2], s));
@@ -511,10 +563,14 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         list = {w.cs.wl.p, reinterpret_cast<const unsigned long long*>(w.cs.nwl.p), nwl_host};
       }
       run_detect_free_lists(da, w.NL, &list, 1, halo_kill_route(w), w.det, w.stats.p, s);
+      rt_mark("detect");
       halo_barrier(w);  // every rank's kills have landed
+      rt_mark("barrier");
       i64* next_cnt = reinterpret_cast<i64*>(w.stats.p + nstats);
       halo_next_worklist(w, w.next_wl.p, next_cnt);
+      rt_mark("next_worklist");
       halo_broadcast_losers(w, w.next_wl.p, next_cnt, w.NL);
+      rt_mark("broadcast_losers");
     } else {
       run_detect(da, w.NL, w.det, w.stats.p, s);
     }

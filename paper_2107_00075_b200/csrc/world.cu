@@ -578,7 +578,7 @@ void world_reset_exchange(World& w) {
 
 void world_exchange_local(World& w, bool changed_only, bool write_all) {
   launch_exchange_local(w.routed.p, w.nrouted, w.st_off.p, w.st_dst.p, w.st_pair.p, w.colors.p,
-                        w.last_sent.p, changed_only, write_all, w.pair_cnt.p, w.stream);
+                        w.last_sent.p, changed_only, write_all, w.pair_cnt.p, (i64)w.P * w.P, w.stream);
 }
 
 }  // namespace chroma

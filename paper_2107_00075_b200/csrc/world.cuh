@@ -49,11 +49,14 @@ struct ColorScratch {
 // Global hub pre-colouring scratch (hubs.cu)
 struct HubScratch {
   DBuf<uint8_t> flags;
-  DBuf<i32> lhubs;
-  DBuf<i64> nlh, lcnt, loff, lgid, lnbr;   // this world's owned hubs
-  DBuf<i64> ggid, gcnt, gnbr;              // all-gathered (connected worlds)
-  DBuf<i64> rowptr, cntz;
-  DBuf<u64> keys;                          // sorted (gid << 32 | H index)
+  DBuf<u32> bits;                          // hub bitmap over local lids
+  DBuf<i32> lhubs, unit_hub;
+  DBuf<i64> nlh, lcnt, loff, lgid, nunits, ustart;  // this world's owned hubs
+  DBuf<i32> lnbr;                          // their hub neighbours (gids)
+  DBuf<i64> ggid, cntz, pad64;             // H order (all ranks)
+  DBuf<i32> gnbr, pad32;
+  DBuf<i64> rowptr;
+  DBuf<i32> table;                         // gid -> H index (hub gids only)
   DBuf<i32> col, colors, list, ovf;
   DBuf<i64> novf;
   DBuf<unsigned long long> missing;

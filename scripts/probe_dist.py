@@ -10,6 +10,7 @@ from paper_2107_00075_b200.dist import DistWorld
 rank, N, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 if rank == 0 and os.environ.get("TRACE0"):
     os.environ["CHROMA_FREE_TRACE"] = "1"
+    os.environ["CHROMA_ROUND_TRACE"] = "1"
 torch.cuda.set_device(local)
 _lib.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
