@@ -1,0 +1,520 @@
+// Level-synchronous Gauss-Seidel first fit on one thread-block cluster.
+//
+// The reference colours the worklist in ascending id (chroma/localcolor.py:161-165):
+// v's colour depends on its worklist neighbours u < v, so the work is a DAG whose
+// longest path (C2 27-point 128^3: 890 levels; a 32-plane slab: 506; C1 grid 1000^2:
+// 1999) bounds any exact evaluation.  The dataflow kernel (color_gs_d1.cu) resolves
+// each level through global-memory flags -- a producer store, an L2 round trip and a
+// poll, about 3 us per level.  Here the levels are walked by ONE cluster of CL CTAs
+// (16 SMs, non-portable cluster size) and the colours live in distributed shared
+// memory, one byte per vertex, dealt to the CTAs in blocks of B = 1024 ids
+// round-robin (block b -> CTA b % CL), so every level's vertices spread evenly over
+// the cluster while mesh neighbours x +- 1, x +- L mostly share a block.  A level
+// costs a few shared / DSMEM gathers, a store and one barrier.cluster.
+//
+// The plan (built once per world together with the level schedule, gs_levels.cu):
+//   * entries: the schedule without padding, level by level, grouped by owner CTA;
+//   * items: each CTA's entries of a level in chunks of at most CAP, with their
+//     rows copied out into fixed-width slots (DW >= max degree, -1 padded) and stored
+//     transposed per item (slot k of entry t at item_base + k * n + t) so a warp's
+//     gathers of one slot are one contiguous read;
+//   * per CTA and level: the first item.
+// A CTA streams its items through S shared-memory stages with cp.async, S - 1 items
+// ahead of the one being coloured (items are static: only the colours are on the
+// dependency chain).  Every CTA colours only vertices it owns, so each colour store
+// is local; neighbours' colours are local or DSMEM loads.  First fit of a row of at
+// most 32 entries is at most 33: a 64-bit mask, colours above 64 never block.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "world.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace chroma {
+namespace {
+
+constexpr int S = 3;  // cp.async stages
+
+__global__ void k_flag_valid(const i32* wl, i64 n, uint8_t* f) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    f[i] = wl[i] >= 0;
+}
+
+struct Own {
+  int logB, logCL;
+  __device__ __forceinline__ int owner(i64 x) const { return (int)((x >> logB) & ((1 << logCL) - 1)); }
+  __device__ __forceinline__ i64 offset(i64 x) const {
+    return ((x >> (logB + logCL)) << logB) | (x & ((1ll << logB) - 1));
+  }
+  __device__ __forceinline__ i32 loc(i64 x) const { return (i32)(((i64)owner(x) << 24) | offset(x)); }
+};
+
+// key of entry j: level << 36 | owner << 32 | id  (sorted: level, owner CTA, id)
+__global__ void k_entry_keys(const i32* v, i64 nent, const i64* lstart, i64 L, Own own, u64* keys) {
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
+    i64 lo = 0, hi = L;  // last level with lstart <= j
+    while (hi - lo > 1) {
+      const i64 mid = (lo + hi) >> 1;
+      if (lstart[mid] <= j) lo = mid;
+      else hi = mid;
+    }
+    keys[j] = ((u64)lo << 36) | ((u64)own.owner(v[j]) << 32) | (u32)v[j];
+  }
+}
+__global__ void k_keys_to_ids(const u64* keys, i64 n, i32* v) {
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x)
+    v[j] = (i32)(keys[j] & 0xffffffffu);
+}
+
+// bounds[l*(CL+1)+r] = first entry of level l owned by CTA >= r
+__global__ void k_bounds(const u64* keys, i64 nent, i64 L, int CL, i64* bounds) {
+  const i64 n = L * (CL + 1);
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i64 l = i / (CL + 1);
+    const int r = (int)(i % (CL + 1));
+    const u64 key = ((u64)l << 36) + ((u64)r << 32);  // r = CL = 16 carries into the level bits
+    i64 lo = 0, hi = nent;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (keys[mid] < key) lo = mid + 1;
+      else hi = mid;
+    }
+    bounds[i] = lo;
+  }
+}
+
+// Slots of an entry: the neighbours whose colour can be non-zero when v is coloured
+// in the protocol's round 0 -- worklist members below v (coloured in earlier levels)
+// and vertices outside the worklist (fixed colours); worklist members above v still
+// hold their pre-call colour, 0 on that path.
+__device__ __forceinline__ bool keep_slot(i32 u, i32 v, const uint8_t* member) { return u < v || !member[u]; }
+
+__global__ void k_slot_count(const i64* rowptr, const i32* col, const i32* v, i64 nent, const uint8_t* member,
+                             unsigned* maxd) {
+  unsigned m = 0;
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
+    const i32 x = v[j];
+    unsigned d = 0;
+    for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) d += keep_slot(col[e], x, member);
+    m = max(m, d);
+  }
+  atomicMax(maxd, m);
+}
+
+__global__ void k_mark(const i32* v, i64 n, uint8_t* member) {
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) member[v[j]] = 1;
+}
+
+// rows of every entry into its item's transposed slots
+__global__ void k_fill_slots(const i64* rowptr, const i32* col, const i32* v, const i32* ent_item,
+                             const i32* item_a, const i32* item_n, i64 nent, int DW, Own own, const uint8_t* member,
+                             i32* nb) {
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
+    const i32 it = ent_item[j];
+    const i64 a = item_a[it], n = item_n[it];
+    const i64 t = j - a;
+    const i32 x = v[j];
+    int k = 0;
+    for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) {
+      const i32 u = col[e];
+      if (keep_slot(u, x, member)) nb[a * DW + (i64)(k++) * n + t] = own.loc(u);
+    }
+    for (; k < DW; k++) nb[a * DW + (i64)k * n + t] = -1;
+  }
+}
+
+__global__ void k_ent_item(const i32* item_a, const i32* item_n, i64 nitems, i32* ent_item) {
+  for (i64 it = blockIdx.x; it < nitems; it += gridDim.x)
+    for (i64 t = threadIdx.x; t < item_n[it]; t += blockDim.x) ent_item[item_a[it] + t] = (i32)it;
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(a), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+struct ClusterArgs {
+  const i32* v;         // entries
+  const i32* nb;        // transposed slots
+  const i32* item_a;    // per item: first entry
+  const i32* item_n;    // per item: entries
+  const i32* cta_item;  // [CL][L+1]: first item (global index) of level l for CTA r
+  i64 L;
+  i64 nv, per;  // per: bytes of colour slice per CTA
+  int DW, CAP;
+  Own own;
+  i32* val;
+  const i32* old;
+  int exp;                  // dev experiments (timing only): 1 no remote loads, 2 no global store, 4 item_n from smem
+  unsigned long long* dbg;  // optional [4] clock sums of CTA 0 (wait, colour, cluster sync, items)
+};
+
+template <int DW>
+__global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int r = (int)cluster.block_rank();
+  const int CL = (int)cluster.num_blocks();
+  const int t = threadIdx.x;
+  const i64 per_pad = (a.per + 15) / 16 * 16;
+  unsigned char* col8 = smem;
+  const i64 stage_bytes = ((i64)a.CAP * (a.DW + 1) + 4) * 4;  // [v x CAP | n, pad x3 | slots]
+  unsigned char* stages = smem + per_pad + 16;
+  const u32 base8 = (u32)__cvta_generic_to_shared(col8);
+  if (t == 0) col8[per_pad] = 0;  // the byte empty slots read
+  // ---- my colour slice: pre-call colours (worklist entries: their old colour)
+  const int lB = a.own.logB, lC = a.own.logCL;
+  for (i64 o = t; o < a.per; o += blockDim.x) {
+    const i64 x = ((((o >> lB) << lC) + r) << lB) | (o & ((1ll << lB) - 1));
+    i32 c = 0;
+    if (x < a.nv) {
+      c = a.val[x];
+      if (c == PENDING) c = a.old ? a.old[x] : 0;
+    }
+    col8[o] = (unsigned char)((c < 0 || c > 255) ? 0 : c);
+  }
+  const i32* my_item = a.cta_item + (i64)r * (a.L + 1);
+  const i32 k_begin = my_item[0], k_end = my_item[a.L];
+  auto issue = [&](i32 k) {
+    if (k < k_end) {
+      unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
+      const i32 ea = a.item_a[k], n = a.item_n[k];
+      i32* sv = reinterpret_cast<i32*>(st);
+      i32* snb = sv + a.CAP + 4;
+      if (t == 0) cp_async4(sv + a.CAP, a.item_n + k);  // n rides with the item
+      for (int i = t; i < n; i += blockDim.x) cp_async4(sv + i, a.v + ea + i);
+      const i32* gnb = a.nb + (i64)ea * a.DW;
+      const int q = n * a.DW / 4;  // n * DW is a multiple of 4 (DW is)
+      for (int i = t; i < q; i += blockDim.x) cp_async16(snb + 4 * i, gnb + 4 * i);
+    }
+    cp_commit();
+  };
+  for (int k = 0; k < S - 1; k++) issue(k_begin + k);
+  cluster.sync();
+  i32 k = k_begin;
+  long long tw = 0, tc = 0, ts = 0, ni = 0;
+  const bool dbg = a.dbg && r == 0 && t == 0;
+  i32 kend_next = my_item[1];
+  for (i64 l = 0; l < a.L; l++) {
+    const i32 kend = kend_next;
+    if (l + 2 <= a.L) kend_next = my_item[l + 2];  // one level ahead (off the chain)
+    if (a.exp & 8) k = kend;
+    for (; k < kend; k++) {
+      const long long c0 = dbg ? clock64() : 0;
+      if (a.exp & 128) {
+        // dev: synchronous staging of item k into its own stage
+        __syncthreads();
+        unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
+        const i32 ea = a.item_a[k], n = a.item_n[k];
+        i32* sv = reinterpret_cast<i32*>(st);
+        i32* snb = sv + a.CAP + 4;
+        for (int i = t; i < n; i += blockDim.x) sv[i] = a.v[ea + i];
+        if (t == 0) sv[a.CAP] = n;
+        for (int i = t; i < n * a.DW; i += blockDim.x) snb[i] = a.nb[(i64)ea * a.DW + i];
+      }
+      cp_wait<S - 2>();
+      __syncthreads();
+      const long long c1 = dbg ? clock64() : 0;
+      if (dbg) tw += c1 - c0, ni++;
+      const unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
+      const i32* sv = reinterpret_cast<const i32*>(st);
+      const i32* snb = sv + a.CAP + 4;
+      const i32 n = sv[a.CAP];
+      if (t < n) {
+        const i32 v = sv[t];
+        // all DW slots at once: every gather of the row is in flight together
+        i32 x[DW];
+#pragma unroll
+        for (int j = 0; j < DW; j++) x[j] = snb[j * n + t];
+        // branch-free: every slot's byte address in the cluster's shared window (mapa),
+        // empty slots read a zero byte of this CTA; all loads issue before any use
+        u32 ad[DW];
+#pragma unroll
+        for (int j = 0; j < DW; j++) {
+          const u32 q = x[j] >= 0 ? (u32)x[j] >> 24 : (u32)r;
+          const u32 off = x[j] >= 0 ? (u32)x[j] & 0xffffffu : (u32)per_pad;
+          asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ad[j]) : "r"(base8 + off), "r"(q));
+        }
+        int c[DW];
+#pragma unroll
+        for (int j = 0; j < DW; j++) asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=r"(c[j]) : "r"(ad[j]));
+        u64 m = 0;
+#pragma unroll
+        for (int j = 0; j < DW; j++)
+          if (c[j] >= 1 && c[j] <= 64) m |= 1ull << (c[j] - 1);
+        const int cv = __ffsll((long long)~m);
+        col8[a.own.offset(v)] = (unsigned char)cv;
+      }
+      __syncthreads();
+      if (dbg) tc += clock64() - c1;
+      issue(k + S - 1);
+    }
+    const long long c2 = dbg ? clock64() : 0;
+    // Level barrier.  The level's colours are shared-memory stores of this CTA,
+    // completed in this SM's shared memory by the item's bar.sync and a CTA fence;
+    // remote readers load them from that shared memory after the barrier.  A
+    // cluster-scope release (fence.acq_rel.cluster / arrive.release) compiles to
+    // MEMBAR.ALL.GPU, which would also drain the cp.async prefetches in flight --
+    // a DRAM round trip per level -- so the arrive is relaxed after a CTA fence.
+    asm volatile("fence.acq_rel.cta;\n\tbarrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" :::
+                     "memory");
+    if (dbg) ts += clock64() - c2;
+  }
+  cp_wait<0>();
+  // colours back to global memory once, at the end (no global stores inside the
+  // level loop for the cluster barriers to drain): worklist entries still read PENDING
+  for (i64 o = t; o < a.per; o += blockDim.x) {
+    const i64 x = ((((o >> lB) << lC) + r) << lB) | (o & ((1ll << lB) - 1));
+    if (x < a.nv && a.val[x] == PENDING) a.val[x] = col8[o];
+  }
+  if (dbg) {
+    a.dbg[0] = tw;
+    a.dbg[1] = tc;
+    a.dbg[2] = ts;
+    a.dbg[3] = ni;
+  }
+}
+
+using ClusterKernel = void (*)(ClusterArgs);
+ClusterKernel cluster_kernel(int DW) {
+  switch (DW) {
+    case 4: return k_gs_cluster<4>;
+    case 8: return k_gs_cluster<8>;
+    case 12: return k_gs_cluster<12>;
+    case 16: return k_gs_cluster<16>;
+    case 20: return k_gs_cluster<20>;
+    case 24: return k_gs_cluster<24>;
+    case 28: return k_gs_cluster<28>;
+    default: return k_gs_cluster<32>;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- plan
+bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
+                        i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s) {
+  plan.ok = false;
+  static const bool disabled = std::getenv("CHROMA_NO_CLUSTER") != nullptr;
+  if (disabled || max_deg > 32 || nv <= 0 || level_n <= 0 || level_sizes.empty()) return false;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  int max_smem = 0;
+  CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // ---- entries: the schedule without its padding (ids ascending within a level)
+  DBuf<uint8_t> f;
+  f.alloc(level_n, s);
+  k_flag_valid<<<grid_for(level_n, 256, num_sms() * 8), 256, 0, s>>>(level_wl, level_n, f.p);
+  count_launch();
+  plan.v.alloc(level_n, s);
+  DBuf<i64> nent_d;
+  nent_d.alloc(1, s);
+  select_flagged_values(level_wl, f.p, level_n, plan.v.p, nent_d.p, s);
+  // worklist membership and the widest pruned row
+  DBuf<uint8_t> member;
+  member.alloc(nv + 1, s);
+  member.zero(s);
+  DBuf<unsigned> maxd;
+  maxd.alloc(1, s);
+  maxd.zero(s);
+  {
+    i64 ne = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&ne, nent_d.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    k_mark<<<grid_for(std::max<i64>(ne, 1), 256, num_sms() * 8), 256, 0, s>>>(plan.v.p, ne, member.p);
+    k_slot_count<<<grid_for(std::max<i64>(ne, 1), 256, num_sms() * 8), 256, 0, s>>>(rowptr, col, plan.v.p, ne,
+                                                                                 member.p, maxd.p);
+    count_launch(2);
+  }
+  unsigned hmaxd = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&hmaxd, maxd.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  const int DW = (int)std::max<i64>(4, ((i64)hmaxd + 3) / 4 * 4);
+  int CL = 0, CAP = 0;
+  i64 per = 0;
+  const int logB = 10;
+  const i64 nblocks = (nv + (1ll << logB) - 1) >> logB;
+  for (int cl : {16, 8}) {
+    per = (nblocks + cl - 1) / cl << logB;  // colour bytes per CTA (whole blocks)
+    const i64 per_pad = (per + 15) / 16 * 16;
+    const i64 room = (i64)max_smem - per_pad - 16 - 1024;
+    if (room <= 0 || per >= (1ll << 24)) continue;
+    i64 cap = (room / (S * 4) - 4) / (DW + 1);
+    cap = std::min<i64>(cap, 1024) / 32 * 32;
+    if (cap < 64) continue;
+    // a cluster of cl CTAs with this much shared memory must be schedulable
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3((unsigned)cap);
+    cfg.dynamicSmemBytes = (size_t)(per_pad + 16 + S * (cap * (DW + 1) + 4) * 4);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const ClusterKernel kf = cluster_kernel(DW);
+    cudaFuncAttributes fa;
+    CUDA_CHECK(cudaFuncGetAttributes(&fa, kf));
+    CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    max_smem - (int)fa.sharedSizeBytes));
+    if (cl > 8) CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kf, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (nclusters < 1) continue;
+    CL = cl;
+    CAP = (int)cap;
+    break;
+  }
+  if (CL == 0) return false;
+  // level boundaries in entry space; entries regrouped by (level, owner CTA, id)
+  std::vector<i64> lstart(1, 0);
+  for (i64 sz : level_sizes) lstart.push_back(lstart.back() + sz);
+  const i64 nent = lstart.back();
+  const i64 L = (i64)lstart.size() - 1;
+  Own own;
+  own.logB = logB;
+  own.logCL = CL == 16 ? 4 : 3;
+  DBuf<i64> ls_d, bnd_d;
+  ls_d.upload(lstart.data(), L + 1, s);
+  DBuf<u64> keys;
+  keys.alloc(std::max<i64>(nent, 1), s);
+  k_entry_keys<<<grid_for(std::max<i64>(nent, 1), 256, num_sms() * 8), 256, 0, s>>>(plan.v.p, nent, ls_d.p, L, own,
+                                                                                    keys.p);
+  sort_u64(keys.p, nent, s);
+  k_keys_to_ids<<<grid_for(std::max<i64>(nent, 1), 256, num_sms() * 8), 256, 0, s>>>(keys.p, nent, plan.v.p);
+  bnd_d.alloc(L * (CL + 1), s);
+  k_bounds<<<grid_for(L * (CL + 1), 256, num_sms() * 8), 256, 0, s>>>(keys.p, nent, L, CL, bnd_d.p);
+  count_launch(3);
+  std::vector<i64> bnd((size_t)(L * (CL + 1)));
+  CUDA_CHECK(cudaMemcpyAsync(bnd.data(), bnd_d.p, sizeof(i64) * bnd.size(), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  // ---- items per CTA, grouped by CTA (each CTA's items are contiguous)
+  std::vector<i32> ia, in, ci((size_t)CL * (L + 1));
+  for (int r = 0; r < CL; r++)
+    for (i64 l = 0; l < L; l++) {
+      ci[(size_t)r * (L + 1) + l] = (i32)ia.size();
+      const i64 b0 = bnd[(size_t)(l * (CL + 1) + r)], b1 = bnd[(size_t)(l * (CL + 1) + r + 1)];
+      for (i64 x = b0; x < b1; x += CAP) {
+        ia.push_back((i32)x);
+        in.push_back((i32)std::min<i64>(CAP, b1 - x));
+      }
+      if (l == L - 1) ci[(size_t)r * (L + 1) + L] = (i32)ia.size();
+    }
+  if (nent >= (1ll << 31) || (i64)ia.size() >= (1ll << 31)) return false;
+  const i64 nitems = (i64)ia.size();
+  plan.item_a.upload(ia.data(), std::max<i64>(nitems, 1), s);
+  plan.item_n.upload(in.data(), std::max<i64>(nitems, 1), s);
+  plan.cta_item.upload(ci.data(), (i64)ci.size(), s);
+  DBuf<i32> ent_item;
+  ent_item.alloc(std::max<i64>(nent, 1), s);
+  k_ent_item<<<(int)std::min<i64>(std::max<i64>(nitems, 1), (i64)num_sms() * 16), 256, 0, s>>>(
+      plan.item_a.p, plan.item_n.p, nitems, ent_item.p);
+  plan.nb.alloc(std::max<i64>(nent * DW, 1), s);
+  k_fill_slots<<<grid_for(std::max<i64>(nent, 1), 256, num_sms() * 8), 256, 0, s>>>(
+      rowptr, col, plan.v.p, ent_item.p, plan.item_a.p, plan.item_n.p, nent, DW, own, member.p, plan.nb.p);
+  count_launch(2);
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  plan.CL = CL;
+  plan.CAP = CAP;
+  plan.DW = DW;
+  plan.per = per;
+  plan.logB = own.logB;
+  plan.logCL = own.logCL;
+  plan.nv = nv;
+  plan.L = L;
+  plan.smem = (size_t)((per + 15) / 16 * 16 + 16 + (i64)S * ((i64)CAP * (DW + 1) + 4) * 4);
+  plan.ok = true;
+  if (const char* dump = std::getenv("CHROMA_CLUSTER_DUMP")) {
+    // dev aid: the plan as raw arrays (n_ent v, n_items a, n, CL*(L+1) cta_item, nent*DW slots)
+    std::vector<i32> hv((size_t)nent), hnb((size_t)(nent * DW));
+    CUDA_CHECK(cudaMemcpy(hv.data(), plan.v.p, sizeof(i32) * nent, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(hnb.data(), plan.nb.p, sizeof(i32) * nent * DW, cudaMemcpyDeviceToHost));
+    if (FILE* fh = std::fopen(dump, "wb")) {
+      const i64 hdr[6] = {nent, nitems, (i64)CL, L, (i64)DW, per};
+      std::fwrite(hdr, sizeof(hdr), 1, fh);
+      std::fwrite(hv.data(), 4, hv.size(), fh);
+      std::fwrite(ia.data(), 4, ia.size(), fh);
+      std::fwrite(in.data(), 4, in.size(), fh);
+      std::fwrite(ci.data(), 4, ci.size(), fh);
+      std::fwrite(hnb.data(), 4, hnb.size(), fh);
+      std::fwrite(lstart.data(), 8, lstart.size(), fh);
+      std::fclose(fh);
+    }
+  }
+  static const bool trace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
+  if (trace)
+    std::fprintf(stderr, "[cluster] %d CTAs x %d threads, %lld levels, %lld entries, %lld items, DW %d, smem %zu\n",
+                 CL, CAP, (long long)L, (long long)nent, (long long)nitems, DW, plan.smem);
+  return true;
+}
+
+void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStream_t s) {
+  ClusterArgs a;
+  a.v = p.v.p;
+  a.nb = p.nb.p;
+  a.item_a = p.item_a.p;
+  a.item_n = p.item_n.p;
+  a.cta_item = p.cta_item.p;
+  a.L = p.L;
+  a.nv = p.nv;
+  a.per = p.per;
+  a.own.logB = p.logB;
+  a.own.logCL = p.logCL;
+  a.DW = p.DW;
+  a.CAP = p.CAP;
+  a.val = val;
+  a.old = old;
+  static const int exp_env = std::getenv("CHROMA_CLUSTER_EXP") ? std::atoi(std::getenv("CHROMA_CLUSTER_EXP")) : 0;
+  a.exp = exp_env;
+  static const bool trace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
+  DBuf<unsigned long long> dbg;
+  a.dbg = nullptr;
+  if (trace) {
+    dbg.alloc(4, s);
+    dbg.zero(s);
+    a.dbg = dbg.p;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(p.CL);
+  cfg.blockDim = dim3((unsigned)p.CAP);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, cluster_kernel(p.DW), a));
+  count_launch();
+  CUDA_CHECK(cudaGetLastError());
+  if (trace) {
+    unsigned long long h[4];
+    CUDA_CHECK(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "[cluster] CTA0 cycles: wait %llu colour %llu cluster-sync %llu over %llu items, %lld levels\n",
+                 h[0], h[1], h[2], h[3], (long long)p.L);
+  }
+}
+
+}  // namespace chroma

@@ -109,11 +109,12 @@ int G(i64 n) { return grid_for(std::max<i64>(n, 1), 256, num_sms() * 16); }
 }  // namespace
 
 bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl, i64 nwl, DBuf<i32>& out,
-                       i64& nout, cudaStream_t s) {
-  static const i64 min_width = [] {
+                       i64& nout, cudaStream_t s, std::vector<i64>* sizes_out, i64 min_width_override) {
+  static const i64 min_width_env = [] {
     const char* e = std::getenv("CHROMA_LEVEL_MIN_WIDTH");
     return e ? std::atoll(e) : 2048ll;
   }();
+  const i64 min_width = min_width_override > 0 ? min_width_override : min_width_env;
   static const bool trace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
   if (nwl < 4096) return false;
   const i64 max_levels = nwl / min_width;
@@ -170,6 +171,7 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   if ((i64)sizes.size() > max_levels) return false;
   CHROMA_REQUIRE(seen == nwl, CHROMA_ERUNTIME, "level schedule did not cover the worklist");
   const i64 L = (i64)sizes.size();
+  if (sizes_out) *sizes_out = sizes;
   if (trace) std::fprintf(stderr, "[levels] %lld levels for %lld vertices\n", (long long)L, (long long)nwl);
   std::vector<i64> start((size_t)L), pstart((size_t)L);
   i64 a = 0, b = 0;

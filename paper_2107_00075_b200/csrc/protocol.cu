@@ -242,7 +242,8 @@ gauss_seidel:
       L.level_mode = S.level_mode;
     }
     if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
-    launch_gs(L, s);
+    if (S.level_wl && S.level_mode && S.cplan && dist == 1 && !L.old) launch_gs_cluster(*S.cplan, L.val, L.old, s);
+    else launch_gs(L, s);
     if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
     if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
     return;
@@ -397,6 +398,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   // owned vertices' sets, uncolouring each loser at its owner (halo_p2p.cu).
   static const bool no_fast = std::getenv("CHROMA_NO_FAST_FREE") != nullptr;
   static const bool no_levels = std::getenv("CHROMA_NO_LEVELS") != nullptr;
+  static const bool no_cluster = std::getenv("CHROMA_NO_CLUSTER") != nullptr;
   // round-0 schedule: 0 auto (levels if the DAG is wide, else rank-interleaved for
   // virtual ranks, else id order), 1 levels only, 2 interleave only, 3 id order
   static const int sched = (int)env_i64("CHROMA_GS_SCHEDULE", 0);
@@ -505,8 +507,18 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         }
         i64 n = 0;
         // levels when the DAG is wide; else (virtual ranks) rank-interleaved id order
+        // bounded degree <= 32: try the cluster kernel (gs_cluster.cu), which walks
+        // narrow levels as cheaply as wide ones; otherwise only wide DAGs take levels
+        const bool try_cluster = w.delta_max <= 32 && !no_cluster;
+        std::vector<i64> lsizes;
         w.level_mode = (sched == 0 || sched == 1) && w.delta_max <= level_max_deg &&
-                       build_level_order(w.g.rowptr.p, w.g.col.p, w.NL, w.cs.wl.p, owned, w.level_wl, n, s);
+                       build_level_order(w.g.rowptr.p, w.g.col.p, w.NL, w.cs.wl.p, owned, w.level_wl, n, s,
+                                         &lsizes, try_cluster ? 1 : -1);
+        if (w.level_mode && try_cluster &&
+            !build_cluster_plan(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, w.level_wl.p, n, lsizes, w.cplan, s)) {
+          // no cluster: keep the schedule only if it is wide enough for the dataflow kernel
+          if ((i64)lsizes.size() * 2048 > owned) w.level_mode = false;
+        }
         w.level_n = w.level_mode ? n : 0;
         if (!w.level_mode && (sched == 0 || sched == 2) &&
             build_rank_interleave(w.cs.wl.p, counts, w.level_wl, n, s))
@@ -518,6 +530,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         w.cs.level_wl = w.level_wl.p;
         w.cs.level_n = w.level_n;
         w.cs.level_mode = w.level_mode;
+        w.cs.cplan = w.level_mode && w.cplan.ok ? &w.cplan : nullptr;
       }
     }
     rt_mark("hubs+worklist");
@@ -525,6 +538,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
               algo, true, w.cs, s, gs_like ? ev[6] : nullptr, gs_like ? ev[7] : nullptr);
     rt_mark("color");
     w.cs.level_wl = nullptr;
+    w.cs.cplan = nullptr;
     w.cs.keep_free = false;
     CUDA_CHECK(cudaEventRecord(ev[1], s));
     // exchange: every ghost takes its owner's colour; accounting is changed-only

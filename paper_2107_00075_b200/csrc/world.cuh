@@ -27,6 +27,15 @@ struct Csr {
   DBuf<i32> col;
 };
 
+// Level-synchronous Gauss-Seidel plan for one thread-block cluster (gs_cluster.cu)
+struct ClusterPlan {
+  bool ok = false;
+  int CL = 0, CAP = 0, DW = 0, logB = 10, logCL = 4;
+  i64 per = 0, nv = 0, L = 0;
+  size_t smem = 0;
+  DBuf<i32> v, nb, item_a, item_n, cta_item;
+};
+
 // Colouring scratch shared by every entry point that colours a CSR.
 struct ColorScratch {
   DBuf<i32> wl, val, old, prop, pend2;
@@ -39,6 +48,7 @@ struct ColorScratch {
   const i32* level_wl = nullptr;
   i64 level_n = 0;
   bool level_mode = true;
+  const ClusterPlan* cplan = nullptr;  // level schedule on one cluster (gs_cluster.cu)
   // free mode: keep the speculative path even without heavy rows (hubs pre-coloured)
   bool keep_free = false;
   DBuf<i64> level_n_dev;
@@ -128,6 +138,7 @@ struct World {
   DBuf<i32> level_wl;
   i64 level_n = -1;
   bool level_mode = false;
+  ClusterPlan cplan;
   // device-side timing of the last run_distributed (CUDA events on `stream`)
   double t_total = 0, t_color_kernel = 0, t_color = 0, t_comm = 0, t_detect = 0;
 
@@ -160,8 +171,18 @@ void halo_release_p2p(World& w);
 
 // Level schedule of a sorted worklist (padded to chunks; false if the DAG is too
 // deep and narrow to benefit).  gs_levels.cu.
+// sizes_out: the (unpadded) size of every level; min_width_override > 0 replaces the
+// minimum average level width (CHROMA_LEVEL_MIN_WIDTH, default 2048).
 bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl, i64 nwl, DBuf<i32>& out,
-                       i64& nout, cudaStream_t s);
+                       i64& nout, cudaStream_t s, std::vector<i64>* sizes_out = nullptr,
+                       i64 min_width_override = -1);
+
+// Level-synchronous Gauss-Seidel on one thread-block cluster (gs_cluster.cu): the
+// plan is built once from a level schedule (bounded degree <= 32, colours of every
+// vertex fit the cluster's shared memory as bytes); false if not applicable.
+bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
+                        i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s);
+void launch_gs_cluster(const ClusterPlan& plan, i32* val, const i32* old, cudaStream_t s);
 
 // Round-robin chunk order over the virtual ranks of a world (rank_counts = owned
 // vertices per rank, contiguous in wl).  gs_levels.cu.
