@@ -152,6 +152,7 @@ struct ClusterArgs {
   const i32* nb;        // transposed slots
   const i32* item_a;    // per item: first entry
   const i32* item_n;    // per item: entries
+  const i32* item_l;    // per item: level
   const i32* cta_item;  // [CL][L+1]: first item (global index) of level l for CTA r
   i64 L;
   i64 nv, per;  // per: bytes of colour slice per CTA
@@ -189,13 +190,15 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
   }
   const i32* my_item = a.cta_item + (i64)r * (a.L + 1);
   const i32 k_begin = my_item[0], k_end = my_item[a.L];
-  auto issue = [&](i32 k) {
+  // item descriptors are read one item ahead of their cp.async issue (the global
+  // load stays off the per-level chain)
+  auto issue = [&](i32 k, i32 ea, i32 n) {
     if (k < k_end) {
       unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
-      const i32 ea = a.item_a[k], n = a.item_n[k];
       i32* sv = reinterpret_cast<i32*>(st);
       i32* snb = sv + a.CAP + 4;
-      if (t == 0) cp_async4(sv + a.CAP, a.item_n + k);  // n rides with the item
+      if (t == 0) cp_async4(sv + a.CAP, a.item_n + k);  // n and the level ride with the item
+      if (t == 0) cp_async4(sv + a.CAP + 1, a.item_l + k);
       for (int i = t; i < n; i += blockDim.x) cp_async4(sv + i, a.v + ea + i);
       const i32* gnb = a.nb + (i64)ea * a.DW;
       const int q = n * a.DW / 4;  // n * DW is a multiple of 4 (DW is)
@@ -203,77 +206,90 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     }
     cp_commit();
   };
-  for (int k = 0; k < S - 1; k++) issue(k_begin + k);
+  for (int k = 0; k < S - 1; k++) {
+    const i32 kk = k_begin + k;
+    issue(kk, kk < k_end ? a.item_a[kk] : 0, kk < k_end ? a.item_n[kk] : 0);
+  }
+  i32 nx_a = k_begin + S - 1 < k_end ? a.item_a[k_begin + S - 1] : 0;
+  i32 nx_n = k_begin + S - 1 < k_end ? a.item_n[k_begin + S - 1] : 0;
   cluster.sync();
-  i32 k = k_begin;
   long long tw = 0, tc = 0, ts = 0, ni = 0;
   const bool dbg = a.dbg && r == 0 && t == 0;
-  i32 kend_next = my_item[1];
-  for (i64 l = 0; l < a.L; l++) {
-    const i32 kend = kend_next;
-    if (l + 2 <= a.L) kend_next = my_item[l + 2];  // one level ahead (off the chain)
-    if (a.exp & 8) k = kend;
-    for (; k < kend; k++) {
-      const long long c0 = dbg ? clock64() : 0;
-      if (a.exp & 128) {
-        // dev: synchronous staging of item k into its own stage
-        __syncthreads();
-        unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
-        const i32 ea = a.item_a[k], n = a.item_n[k];
-        i32* sv = reinterpret_cast<i32*>(st);
-        i32* snb = sv + a.CAP + 4;
-        for (int i = t; i < n; i += blockDim.x) sv[i] = a.v[ea + i];
-        if (t == 0) sv[a.CAP] = n;
-        for (int i = t; i < n * a.DW; i += blockDim.x) snb[i] = a.nb[(i64)ea * a.DW + i];
-      }
-      cp_wait<S - 2>();
-      __syncthreads();
-      const long long c1 = dbg ? clock64() : 0;
-      if (dbg) tw += c1 - c0, ni++;
-      const unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
-      const i32* sv = reinterpret_cast<const i32*>(st);
-      const i32* snb = sv + a.CAP + 4;
-      const i32 n = sv[a.CAP];
-      if (t < n) {
-        const i32 v = sv[t];
-        // all DW slots at once: every gather of the row is in flight together
-        i32 x[DW];
-#pragma unroll
-        for (int j = 0; j < DW; j++) x[j] = snb[j * n + t];
-        // branch-free: every slot's byte address in the cluster's shared window (mapa),
-        // empty slots read a zero byte of this CTA; all loads issue before any use
-        u32 ad[DW];
-#pragma unroll
-        for (int j = 0; j < DW; j++) {
-          const u32 q = x[j] >= 0 ? (u32)x[j] >> 24 : (u32)r;
-          const u32 off = x[j] >= 0 ? (u32)x[j] & 0xffffffu : (u32)per_pad;
-          asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ad[j]) : "r"(base8 + off), "r"(q));
-        }
-        int c[DW];
-#pragma unroll
-        for (int j = 0; j < DW; j++) asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=r"(c[j]) : "r"(ad[j]));
-        u64 m = 0;
-#pragma unroll
-        for (int j = 0; j < DW; j++)
-          if (c[j] >= 1 && c[j] <= 64) m |= 1ull << (c[j] - 1);
-        const int cv = __ffsll((long long)~m);
-        col8[a.own.offset(v)] = (unsigned char)cv;
-      }
-      __syncthreads();
-      if (dbg) tc += clock64() - c1;
-      issue(k + S - 1);
+  // Level barriers, split and item-driven.  Every CTA passes L barriers (one per
+  // level), in order; it arrives at level l's barrier once its stores of level l are
+  // done and waits only right before its first gathers of a later level, so stage
+  // hand-off, slot loads and address arithmetic overlap the barrier.  Items carry
+  // their level, so the loop needs no per-level metadata from global memory.  The
+  // colours are shared-memory stores of this CTA, completed in this SM's shared
+  // memory by a CTA fence before the arrive; remote readers load them from there
+  // after the wait.  A cluster-scope release (fence.acq_rel.cluster /
+  // arrive.release) compiles to MEMBAR.ALL.GPU, which would also drain the cp.async
+  // prefetches in flight -- a DRAM round trip per level -- so the arrive is relaxed.
+  bool waiting = false;  // arrived at the last barrier, not yet waited
+  i64 cur = 0;           // barriers arrived at
+  auto wait_level = [&]() {
+    if (waiting) {
+      const long long c2 = dbg ? clock64() : 0;
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      if (dbg) ts += clock64() - c2;
+      waiting = false;
     }
-    const long long c2 = dbg ? clock64() : 0;
-    // Level barrier.  The level's colours are shared-memory stores of this CTA,
-    // completed in this SM's shared memory by the item's bar.sync and a CTA fence;
-    // remote readers load them from that shared memory after the barrier.  A
-    // cluster-scope release (fence.acq_rel.cluster / arrive.release) compiles to
-    // MEMBAR.ALL.GPU, which would also drain the cp.async prefetches in flight --
-    // a DRAM round trip per level -- so the arrive is relaxed after a CTA fence.
-    asm volatile("fence.acq_rel.cta;\n\tbarrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" :::
-                     "memory");
-    if (dbg) ts += clock64() - c2;
+  };
+  auto close_levels_below = [&](i64 lv) {
+    while (cur < lv) {
+      wait_level();
+      asm volatile("fence.acq_rel.cta;\n\tbarrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      waiting = true;
+      cur++;
+    }
+  };
+  for (i32 k = k_begin; k < k_end; k++) {
+    const long long c0 = dbg ? clock64() : 0;
+    cp_wait<S - 2>();
+    __syncthreads();  // stage k landed; every thread is past item k - 1
+    const long long c1 = dbg ? clock64() : 0;
+    if (dbg) tw += c1 - c0, ni++;
+    const unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
+    const i32* sv = reinterpret_cast<const i32*>(st);
+    const i32* snb = sv + a.CAP + 4;
+    const i32 n = sv[a.CAP];
+    const i32 lk = sv[a.CAP + 1];
+    close_levels_below(lk);  // this CTA's stores of every earlier level are out
+    const bool act = t < n;
+    i32 v = 0;
+    // every slot's byte address in the cluster's shared window (mapa); empty slots
+    // read a zero byte of this CTA
+    u32 ad[DW];
+    if (act) {
+      v = sv[t];
+#pragma unroll
+      for (int j = 0; j < DW; j++) {
+        const i32 x = snb[j * n + t];
+        const u32 q = x >= 0 ? (u32)x >> 24 : (u32)r;
+        const u32 off = x >= 0 ? (u32)x & 0xffffffu : (u32)per_pad;
+        asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ad[j]) : "r"(base8 + off), "r"(q));
+      }
+    }
+    wait_level();  // every level below lk is complete everywhere
+    if (act) {
+      int c[DW];
+#pragma unroll
+      for (int j = 0; j < DW; j++) asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=r"(c[j]) : "r"(ad[j]));
+      u64 m = 0;
+#pragma unroll
+      for (int j = 0; j < DW; j++)
+        if (c[j] >= 1 && c[j] <= 64) m |= 1ull << (c[j] - 1);
+      col8[a.own.offset(v)] = (unsigned char)__ffsll((long long)~m);
+    }
+    if (dbg) tc += clock64() - c1;
+    issue(k + S - 1, nx_a, nx_n);  // into item k - 1's stage (all threads are past it)
+    if (k + S < k_end) {
+      nx_a = a.item_a[k + S];
+      nx_n = a.item_n[k + S];
+    }
   }
+  close_levels_below(a.L);
+  wait_level();
   cp_wait<0>();
   // colours back to global memory once, at the end (no global stores inside the
   // level loop for the cluster barriers to drain): worklist entries still read PENDING
@@ -408,7 +424,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   CUDA_CHECK(cudaMemcpyAsync(bnd.data(), bnd_d.p, sizeof(i64) * bnd.size(), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
   // ---- items per CTA, grouped by CTA (each CTA's items are contiguous)
-  std::vector<i32> ia, in, ci((size_t)CL * (L + 1));
+  std::vector<i32> ia, in, il, ci((size_t)CL * (L + 1));
   for (int r = 0; r < CL; r++)
     for (i64 l = 0; l < L; l++) {
       ci[(size_t)r * (L + 1) + l] = (i32)ia.size();
@@ -416,6 +432,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
       for (i64 x = b0; x < b1; x += CAP) {
         ia.push_back((i32)x);
         in.push_back((i32)std::min<i64>(CAP, b1 - x));
+        il.push_back((i32)l);
       }
       if (l == L - 1) ci[(size_t)r * (L + 1) + L] = (i32)ia.size();
     }
@@ -423,6 +440,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   const i64 nitems = (i64)ia.size();
   plan.item_a.upload(ia.data(), std::max<i64>(nitems, 1), s);
   plan.item_n.upload(in.data(), std::max<i64>(nitems, 1), s);
+  plan.item_l.upload(il.data(), std::max<i64>(nitems, 1), s);
   plan.cta_item.upload(ci.data(), (i64)ci.size(), s);
   DBuf<i32> ent_item;
   ent_item.alloc(std::max<i64>(nent, 1), s);
@@ -473,6 +491,7 @@ void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStrea
   a.nb = p.nb.p;
   a.item_a = p.item_a.p;
   a.item_n = p.item_n.p;
+  a.item_l = p.item_l.p;
   a.cta_item = p.cta_item.p;
   a.L = p.L;
   a.nv = p.nv;

@@ -33,7 +33,7 @@ struct ClusterPlan {
   int CL = 0, CAP = 0, DW = 0, logB = 10, logCL = 4;
   i64 per = 0, nv = 0, L = 0;
   size_t smem = 0;
-  DBuf<i32> v, nb, item_a, item_n, cta_item;
+  DBuf<i32> v, nb, item_a, item_n, item_l, cta_item;
 };
 
 // Colouring scratch shared by every entry point that colours a CSR.
