@@ -342,7 +342,7 @@ def main():
     if N == 1 and wl.name == "c2" and args.L == 128 and wl.algorithm == "gauss-seidel":
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-                traffic = json.load(fh)["gs_d1_kernel_c2_p1"]["dram_bytes_per_launch"]
+                traffic = json.load(fh)["colour_kernel_c2_p1"]["dram_bytes_per_launch"]
         except Exception:
             traffic = None
     # ---- end to end through the public API with host buffers
@@ -388,8 +388,9 @@ def main():
                            "l2": f"inputs larger than L2 (int32 col {4 * len(g.col_indices) / 1e6:.0f} MB)"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
-                             "kernel": ("gs_d1_kernel (colouring)" if wl.algorithm == "gauss-seidel"
-                                        else "round-0 colour phase"),
+                             "kernel": ("Gauss-Seidel colouring kernel (k_gs_cluster: level-synchronous, one "
+                                        "16-CTA cluster, colours in DSMEM)" if wl.algorithm == "gauss-seidel"
+                                        else "round-0 colour phase (hub waves + light/tiny passes)"),
                              "algorithmic_bytes_per_launch": B, "kernel_ms": kernel_s * 1e3,
                              "peak_kind": peak_kind},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
