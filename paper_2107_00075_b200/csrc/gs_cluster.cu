@@ -93,14 +93,33 @@ __global__ void k_bounds(const u64* keys, i64 nent, i64 L, int CL, i64* bounds) 
 // and vertices outside the worklist (fixed colours); worklist members above v still
 // hold their pre-call colour, 0 on that path.
 __device__ __forceinline__ bool keep_slot(i32 u, i32 v, const uint8_t* member) { return u < v || !member[u]; }
+constexpr i32 LINK = 1 << 30, PREV = 1 << 29, ID_MASK = PREV - 1;  // entry flags (run links)
 
+// level-ordered entries: is entry j's predecessor x - 1 on the same level (a run link)?
+__device__ __forceinline__ bool same_level_prev(const i32* v, i64 j, const i64* lstart, i64 L) {
+  if (j == 0 || v[j - 1] != v[j] - 1) return false;
+  i64 lo = 0, hi = L;  // last level with lstart <= j
+  while (hi - lo > 1) {
+    const i64 mid = (lo + hi) >> 1;
+    if (lstart[mid] <= j) lo = mid;
+    else hi = mid;
+  }
+  return lstart[lo] < j;
+}
+
+// widest pruned row; the x - 1 slot of a run link is not a slot (the kernel takes
+// that colour from the scan or, at an item start, from its own shared memory)
 __global__ void k_slot_count(const i64* rowptr, const i32* col, const i32* v, i64 nent, const uint8_t* member,
-                             unsigned* maxd) {
+                             const i64* lstart, i64 L, bool chains, unsigned* maxd) {
   unsigned m = 0;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
     const i32 x = v[j];
+    const bool link = chains && same_level_prev(v, j, lstart, L);
     unsigned d = 0;
-    for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) d += keep_slot(col[e], x, member);
+    for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) {
+      const i32 u = col[e];
+      d += keep_slot(u, x, member) && !(link && u == x - 1);
+    }
     m = max(m, d);
   }
   atomicMax(maxd, m);
@@ -110,21 +129,32 @@ __global__ void k_mark(const i32* v, i64 n, uint8_t* member) {
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) member[v[j]] = 1;
 }
 
-// rows of every entry into its item's transposed slots
-__global__ void k_fill_slots(const i64* rowptr, const i32* col, const i32* v, const i32* ent_item,
+// rows of every entry into its item's transposed slots.  Entries are sorted by
+// (level, owner, id) (keys); an adjacent x - 1 on the same level is a run link
+// (gs_levels.cu): it gets no slot, and the entry id carries LINK (x - 1 is the
+// previous entry of this item: the prefix scan supplies its colour) or PREV (x - 1
+// ended this CTA's previous item of the level: read from own shared memory).
+__global__ void k_fill_slots(const i64* rowptr, const i32* col, const u64* keys, const i32* ent_item,
                              const i32* item_a, const i32* item_n, i64 nent, int DW, Own own, const uint8_t* member,
-                             i32* nb) {
+                             i32* nb, i32* v) {
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
     const i32 it = ent_item[j];
     const i64 a = item_a[it], n = item_n[it];
     const i64 t = j - a;
-    const i32 x = v[j];
+    const i32 x = (i32)(keys[j] & 0xffffffffu);
+    const bool cand = j > 0 && (keys[j - 1] >> 36) == (keys[j] >> 36) && (i32)(keys[j - 1] & 0xffffffffu) == x - 1;
+    bool adj = false;
     int k = 0;
     for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) {
       const i32 u = col[e];
+      if (cand && u == x - 1) {
+        adj = true;
+        continue;
+      }
       if (keep_slot(u, x, member)) nb[a * DW + (i64)(k++) * n + t] = own.loc(u);
     }
     for (; k < DW; k++) nb[a * DW + (i64)k * n + t] = -1;
+    v[j] = x | (adj ? (t > 0 ? LINK : PREV) : 0);
   }
 }
 
@@ -157,6 +187,7 @@ struct ClusterArgs {
   i64 L;
   i64 nv, per;  // per: bytes of colour slice per CTA
   int DW, CAP;
+  bool chains;  // the schedule holds runs: entries may carry LINK / PREV
   Own own;
   i32* val;
   const i32* old;
@@ -257,11 +288,15 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     close_levels_below(lk);  // this CTA's stores of every earlier level are out
     const bool act = t < n;
     i32 v = 0;
+    bool linked = false, prev = false;  // run link: x - 1 is the previous entry (LINK, PREV)
     // every slot's byte address in the cluster's shared window (mapa); empty slots
     // read a zero byte of this CTA
     u32 ad[DW];
     if (act) {
       v = sv[t];
+      linked = (v & LINK) != 0;
+      prev = (v & PREV) != 0;
+      v &= ID_MASK;
 #pragma unroll
       for (int j = 0; j < DW; j++) {
         const i32 x = snb[j * n + t];
@@ -271,6 +306,10 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
       }
     }
     wait_level();  // every level below lk is complete everywhere
+    // first fit against the gathered colours: m0, and m1 (next free) for a run link.
+    // Entry t's colour is f_t(colour of t - 1) with f_t(c) = c == p ? a : b; an
+    // unlinked entry is the constant map (p = 0, colours are >= 1).
+    int fp = 0, fa = 0, fb = 0;
     if (act) {
       int c[DW];
 #pragma unroll
@@ -279,8 +318,46 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
 #pragma unroll
       for (int j = 0; j < DW; j++)
         if (c[j] >= 1 && c[j] <= 64) m |= 1ull << (c[j] - 1);
-      col8[a.own.offset(v)] = (unsigned char)__ffsll((long long)~m);
+      if (prev) {
+        const int cp = col8[a.own.offset(v - 1)];
+        if (cp >= 1 && cp <= 64) m |= 1ull << (cp - 1);
+      }
+      const int m0 = __ffsll((long long)~m);
+      fa = fb = m0;
+      if (linked) {
+        fp = m0;
+        fa = __ffsll((long long)(~m & ~(1ull << (m0 - 1))));
+      }
     }
+    if (a.chains && __syncthreads_or(linked)) {
+      // runs: inclusive scan of map composition over the item (g o f = (f.p, g(f.a), g(f.b)))
+      const int lane = t & 31, w = t >> 5;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int qp = __shfl_up_sync(0xffffffffu, fp, o);
+        const int qa = __shfl_up_sync(0xffffffffu, fa, o);
+        const int qb = __shfl_up_sync(0xffffffffu, fb, o);
+        if (lane >= o) {
+          const int na = qa == fp ? fa : fb, nb = qb == fp ? fa : fb;
+          fp = qp, fa = na, fb = nb;
+        }
+      }
+      // across warps: entry 0 is unlinked, so the prefix of warps < w is a
+      // constant reached from the nearest constant warp total
+      int* tot = reinterpret_cast<int*>(stages + (i64)S * stage_bytes);
+      if (lane == 31) {
+        tot[3 * w] = fp, tot[3 * w + 1] = fa, tot[3 * w + 2] = fb;
+      }
+      __syncthreads();
+      if (w > 0 && fp != 0) {
+        int k = w - 1;
+        while (tot[3 * k] != 0) k--;
+        int cc = tot[3 * k + 2];
+        for (k++; k < w; k++) cc = cc == tot[3 * k] ? tot[3 * k + 1] : tot[3 * k + 2];
+        fb = cc == fp ? fa : fb;
+      }
+    }
+    if (act) col8[a.own.offset(v)] = (unsigned char)fb;
     if (dbg) tc += clock64() - c1;
     issue(k + S - 1, nx_a, nx_n);  // into item k - 1's stage (all threads are past it)
     if (k + S < k_end) {
@@ -323,7 +400,8 @@ ClusterKernel cluster_kernel(int DW) {
 
 // ---------------------------------------------------------------- plan
 bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
-                        i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s) {
+                        i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s,
+                        bool chains) {
   plan.ok = false;
   static const bool disabled = std::getenv("CHROMA_NO_CLUSTER") != nullptr;
   if (disabled || max_deg > 32 || nv <= 0 || level_n <= 0 || level_sizes.empty()) return false;
@@ -347,13 +425,22 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   DBuf<unsigned> maxd;
   maxd.alloc(1, s);
   maxd.zero(s);
+  // level boundaries in entry space
+  std::vector<i64> lstart(1, 0);
+  for (i64 sz : level_sizes) lstart.push_back(lstart.back() + sz);
+  const i64 nent = lstart.back();
+  const i64 L = (i64)lstart.size() - 1;
+  if (chains && nv >= PREV) return false;
+  DBuf<i64> ls_d;
+  ls_d.upload(lstart.data(), L + 1, s);
   {
     i64 ne = 0;
     CUDA_CHECK(cudaMemcpyAsync(&ne, nent_d.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
     k_mark<<<grid_for(std::max<i64>(ne, 1), 256, num_sms() * 8), 256, 0, s>>>(plan.v.p, ne, member.p);
-    k_slot_count<<<grid_for(std::max<i64>(ne, 1), 256, num_sms() * 8), 256, 0, s>>>(rowptr, col, plan.v.p, ne,
-                                                                                 member.p, maxd.p);
+    CHROMA_REQUIRE(ne == nent, CHROMA_ERUNTIME, "cluster plan: schedule size mismatch");
+    k_slot_count<<<grid_for(std::max<i64>(ne, 1), 256, num_sms() * 8), 256, 0, s>>>(
+        rowptr, col, plan.v.p, ne, member.p, ls_d.p, L, chains, maxd.p);
     count_launch(2);
   }
   unsigned hmaxd = 0;
@@ -367,7 +454,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   for (int cl : {16, 8}) {
     per = (nblocks + cl - 1) / cl << logB;  // colour bytes per CTA (whole blocks)
     const i64 per_pad = (per + 15) / 16 * 16;
-    const i64 room = (i64)max_smem - per_pad - 16 - 1024;
+    const i64 room = (i64)max_smem - per_pad - 16 - 1024 - 32 * 12;
     if (room <= 0 || per >= (1ll << 24)) continue;
     i64 cap = (room / (S * 4) - 4) / (DW + 1);
     cap = std::min<i64>(cap, 1024) / 32 * 32;
@@ -381,7 +468,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(cl);
     cfg.blockDim = dim3((unsigned)cap);
-    cfg.dynamicSmemBytes = (size_t)(per_pad + 16 + S * (cap * (DW + 1) + 4) * 4);
+    cfg.dynamicSmemBytes = (size_t)(per_pad + 16 + S * (cap * (DW + 1) + 4) * 4 + 32 * 12);
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const ClusterKernel kf = cluster_kernel(DW);
@@ -401,16 +488,11 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
     break;
   }
   if (CL == 0) return false;
-  // level boundaries in entry space; entries regrouped by (level, owner CTA, id)
-  std::vector<i64> lstart(1, 0);
-  for (i64 sz : level_sizes) lstart.push_back(lstart.back() + sz);
-  const i64 nent = lstart.back();
-  const i64 L = (i64)lstart.size() - 1;
+  // entries regrouped by (level, owner CTA, id)
   Own own;
   own.logB = logB;
   own.logCL = CL == 16 ? 4 : 3;
-  DBuf<i64> ls_d, bnd_d;
-  ls_d.upload(lstart.data(), L + 1, s);
+  DBuf<i64> bnd_d;
   DBuf<u64> keys;
   keys.alloc(std::max<i64>(nent, 1), s);
   k_entry_keys<<<grid_for(std::max<i64>(nent, 1), 256, num_sms() * 8), 256, 0, s>>>(plan.v.p, nent, ls_d.p, L, own,
@@ -448,10 +530,11 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
       plan.item_a.p, plan.item_n.p, nitems, ent_item.p);
   plan.nb.alloc(std::max<i64>(nent * DW, 1), s);
   k_fill_slots<<<grid_for(std::max<i64>(nent, 1), 256, num_sms() * 8), 256, 0, s>>>(
-      rowptr, col, plan.v.p, ent_item.p, plan.item_a.p, plan.item_n.p, nent, DW, own, member.p, plan.nb.p);
+      rowptr, col, keys.p, ent_item.p, plan.item_a.p, plan.item_n.p, nent, DW, own, member.p, plan.nb.p, plan.v.p);
   count_launch(2);
   CUDA_CHECK(cudaStreamSynchronize(s));
   plan.CL = CL;
+  plan.chains = chains;
   plan.CAP = CAP;
   plan.DW = DW;
   plan.per = per;
@@ -459,7 +542,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   plan.logCL = own.logCL;
   plan.nv = nv;
   plan.L = L;
-  plan.smem = (size_t)((per + 15) / 16 * 16 + 16 + (i64)S * ((i64)CAP * (DW + 1) + 4) * 4);
+  plan.smem = (size_t)((per + 15) / 16 * 16 + 16 + (i64)S * ((i64)CAP * (DW + 1) + 4) * 4 + 32 * 12);
   plan.ok = true;
   if (const char* dump = std::getenv("CHROMA_CLUSTER_DUMP")) {
     // dev aid: the plan as raw arrays (n_ent v, n_items a, n, CL*(L+1) cta_item, nent*DW slots)
@@ -480,8 +563,8 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   }
   static const bool trace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
   if (trace)
-    std::fprintf(stderr, "[cluster] %d CTAs x %d threads, %lld levels, %lld entries, %lld items, DW %d, smem %zu\n",
-                 CL, CAP, (long long)L, (long long)nent, (long long)nitems, DW, plan.smem);
+    std::fprintf(stderr, "[cluster] %d CTAs x %d threads, %lld levels, %lld entries, %lld items, DW %d, smem %zu%s\n",
+                 CL, CAP, (long long)L, (long long)nent, (long long)nitems, DW, plan.smem, chains ? ", runs" : "");
   return true;
 }
 
@@ -500,6 +583,7 @@ void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStrea
   a.own.logCL = p.logCL;
   a.DW = p.DW;
   a.CAP = p.CAP;
+  a.chains = p.chains;
   a.val = val;
   a.old = old;
   static const int exp_env = std::getenv("CHROMA_CLUSTER_EXP") ? std::atoi(std::getenv("CHROMA_CLUSTER_EXP")) : 0;

@@ -104,12 +104,147 @@ __global__ void k_mark_members(const i32* wl, i64 n, uint8_t* member) {
     member[wl[i]] = 1;
 }
 
+// ---- chain mode (cluster kernel only).  A "run" is a maximal interval of worklist
+// ids h..t inside one 1024-id block (one owner CTA of gs_cluster.cu) in which every
+// v > h is adjacent to v - 1.  Given every other lower neighbour's colour, first fit
+// along a run is a composition of maps c -> (c == m0 ? m1 : m0) (m0, m1 = the two
+// smallest colours free of the others), which the cluster kernel resolves by a
+// prefix scan inside one level.  So a whole run takes one level:
+// level(run) = 1 + max level(run') over runs holding a lower worklist neighbour of
+// a member.  (Runs are id intervals, so the contracted graph is still a DAG; a run
+// holds no edge other than its x - 1 links, see k_chain_cut.)  On
+// the 27-point stencil the runs are the x-rows: 890 -> 382 levels at 128^3.
+__global__ void k_chain_cont(const i64* rowptr, const i32* col, const i32* wl, i64 n, const uint8_t* member,
+                             uint8_t* cont) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = wl[i];
+    bool c = false;
+    if ((v & 1023) != 0 && member[v - 1])
+      for (i64 e = rowptr[v + 1] - 1; e >= rowptr[v]; e--) {  // sorted row: v - 1 is the top lower entry
+        const i32 u = col[e];
+        if (u < v) {
+          c = u == v - 1;
+          break;
+        }
+      }
+    cont[v] = c;
+  }
+}
+
+// one CTA of 1024 threads per 1024-id block: head[x] = the last non-continuation id
+// <= x (a max-scan); runlen[head] = length of the run
+__global__ void __launch_bounds__(1024) k_run_heads(i64 nv, const uint8_t* member, const uint8_t* cont, i32* head,
+                                                    i32* runlen) {
+  __shared__ int wmax[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const i64 x = blockIdx.x * 1024ll + t;
+  const bool c = x < nv && cont[x];
+  int m = c ? -1 : t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, m, o);
+    if (lane >= o) m = max(m, y);
+  }
+  if (lane == 31) wmax[w] = m;
+  __syncthreads();
+  int pre = -1;
+  for (int k = 0; k < w; k++) pre = max(pre, wmax[k]);
+  m = max(m, pre);
+  __syncthreads();
+  if (x < nv && member[x]) {
+    const i32 h = (i32)(blockIdx.x * 1024ll + m);
+    head[x] = h;
+    const bool last = x + 1 >= nv || (t == 1023) || !cont[x + 1];
+    if (last) runlen[h] = (i32)(x - h + 1);
+  }
+}
+
+// the scan resolves only the x - 1 link: a run is cut at x if x has another lower
+// neighbour inside its run (u in [head, x - 2]); cutting there leaves every
+// remaining run free of such edges
+__global__ void k_chain_cut(const i64* rowptr, const i32* col, const i32* wl, i64 n, const i32* head,
+                            uint8_t* cont) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 x = wl[i];
+    if (!cont[x]) continue;
+    const i32 h = head[x];
+    for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) {
+      const i32 u = col[e];
+      if (u >= x - 1) break;
+      if (u >= h) {
+        cont[x] = 0;
+        break;
+      }
+    }
+  }
+}
+
+// indeg[head] = lower worklist neighbours of the run's members outside the run
+__global__ void k_run_indeg(const i64* rowptr, const i32* col, const i32* wl, i64 n, const uint8_t* member,
+                            const i32* head, i32* indeg) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 x = wl[i];
+    const i32 h = head[x];
+    int d = 0;
+    for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) {
+      const i32 u = col[e];
+      if (u >= h) break;
+      d += member[u];
+    }
+    if (d) atomicAdd(indeg + h, d);
+  }
+}
+
+__device__ __forceinline__ void expand_run(i32 h, i32 len, i32 lvl, i32* level, i32* out,
+                                           unsigned long long* nout) {
+  const unsigned long long b = atomicAdd(nout, (unsigned long long)len);
+  for (i32 k = 0; k < len; k++) {
+    out[b + k] = h + k;
+    level[h + k] = lvl;
+  }
+}
+
+__global__ void k_run_sources(const i32* wl, i64 n, const uint8_t* cont, const i32* indeg, const i32* runlen,
+                              i32* level, i32* frontier, unsigned long long* nfront) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = wl[i];
+    if (!cont[v] && indeg[v] == 0) expand_run(v, runlen[v], 0, level, frontier, nfront);
+  }
+}
+
+// as k_level_step over runs: a run is released when its last outside dependency is
+__global__ void k_run_step(const i64* rowptr, const i32* col, const uint8_t* member, const i32* head,
+                           const i32* runlen, const i32* frontier, unsigned long long* cnt, i64 lvl, i32* indeg,
+                           i32* level, i32* next, unsigned long long* sizes) {
+  const int lane = threadIdx.x & 31;
+  const i64 n = (i64)cnt[lvl % 3];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sizes[lvl] = (unsigned long long)n;
+    cnt[(lvl + 2) % 3] = 0;
+  }
+  unsigned long long* nnext = cnt + (lvl + 1) % 3;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 i = warp; i < n; i += nwarps) {
+    const i32 v = frontier[i];
+    const i32 hv = head[v];
+    const i64 rs = rowptr[v], re = rowptr[v + 1];
+    for (i64 e = re - 1 - lane; e >= rs; e -= 32) {
+      const i32 x = col[e];
+      if (x <= v) break;
+      if (!member[x]) continue;
+      const i32 h = head[x];
+      if (h != hv && atomicSub(indeg + h, 1) == 1) expand_run(h, runlen[h], (i32)lvl + 1, level, next, nnext);
+    }
+  }
+}
+
 int G(i64 n) { return grid_for(std::max<i64>(n, 1), 256, num_sms() * 16); }
 
 }  // namespace
 
 bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl, i64 nwl, DBuf<i32>& out,
-                       i64& nout, cudaStream_t s, std::vector<i64>* sizes_out, i64 min_width_override) {
+                       i64& nout, cudaStream_t s, std::vector<i64>* sizes_out, i64 min_width_override, bool chains) {
   static const i64 min_width_env = [] {
     const char* e = std::getenv("CHROMA_LEVEL_MIN_WIDTH");
     return e ? std::atoll(e) : 2048ll;
@@ -129,10 +264,28 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   fb.alloc(nwl, s);
   cnt.alloc(3, s);
   cnt.zero(s);
+  DBuf<uint8_t> cont;
+  DBuf<i32> head, runlen;
   k_mark_members<<<G(nwl), 256, 0, s>>>(wl, nwl, member.p);
-  k_level_indeg<<<grid_for(nwl, 256, num_sms() * 8), 256, 0, s>>>(rowptr, col, wl, nwl, member.p, indeg.p,
-                                                                   level.p, fa.p, cnt.p);
-  count_launch(2);
+  count_launch();
+  if (chains) {
+    cont.alloc(nv + 1, s);
+    cont.zero(s);
+    head.alloc(nv + 1, s);
+    runlen.alloc(nv + 1, s);
+    CUDA_CHECK(cudaMemsetAsync(indeg.p, 0, sizeof(i32) * (size_t)(nv + 1), s));
+    k_chain_cont<<<G(nwl), 256, 0, s>>>(rowptr, col, wl, nwl, member.p, cont.p);
+    k_run_heads<<<(unsigned)((nv + 1023) / 1024), 1024, 0, s>>>(nv, member.p, cont.p, head.p, runlen.p);
+    k_chain_cut<<<G(nwl), 256, 0, s>>>(rowptr, col, wl, nwl, head.p, cont.p);
+    k_run_heads<<<(unsigned)((nv + 1023) / 1024), 1024, 0, s>>>(nv, member.p, cont.p, head.p, runlen.p);
+    k_run_indeg<<<G(nwl), 256, 0, s>>>(rowptr, col, wl, nwl, member.p, head.p, indeg.p);
+    k_run_sources<<<G(nwl), 256, 0, s>>>(wl, nwl, cont.p, indeg.p, runlen.p, level.p, fa.p, cnt.p);
+    count_launch(6);
+  } else {
+    k_level_indeg<<<grid_for(nwl, 256, num_sms() * 8), 256, 0, s>>>(rowptr, col, wl, nwl, member.p, indeg.p,
+                                                                     level.p, fa.p, cnt.p);
+    count_launch();
+  }
   // frontier sizes land in a device array; the host checks every BATCH levels
   constexpr int BATCH = 64;
   const i64 cap_levels = max_levels + BATCH + 1;
@@ -148,8 +301,12 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   while (!done) {
     for (int k = 0; k < BATCH; k++, lvl++) {
       const int p = (int)(lvl & 1);
-      k_level_step<<<grid, 256, 0, s>>>(rowptr, col, member.p, buf[p], cnt.p, lvl, indeg.p, level.p, buf[p ^ 1],
-                                        dsz.p);
+      if (chains)
+        k_run_step<<<grid, 256, 0, s>>>(rowptr, col, member.p, head.p, runlen.p, buf[p], cnt.p, lvl, indeg.p,
+                                        level.p, buf[p ^ 1], dsz.p);
+      else
+        k_level_step<<<grid, 256, 0, s>>>(rowptr, col, member.p, buf[p], cnt.p, lvl, indeg.p, level.p,
+                                          buf[p ^ 1], dsz.p);
     }
     count_launch(BATCH);
     CUDA_CHECK(cudaMemcpyAsync(hsz.data(), dsz.p, sizeof(unsigned long long) * (size_t)lvl, cudaMemcpyDeviceToHost,
@@ -172,7 +329,9 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   CHROMA_REQUIRE(seen == nwl, CHROMA_ERUNTIME, "level schedule did not cover the worklist");
   const i64 L = (i64)sizes.size();
   if (sizes_out) *sizes_out = sizes;
-  if (trace) std::fprintf(stderr, "[levels] %lld levels for %lld vertices\n", (long long)L, (long long)nwl);
+  if (trace)
+    std::fprintf(stderr, "[levels] %lld levels for %lld vertices%s\n", (long long)L, (long long)nwl,
+                 chains ? " (runs)" : "");
   std::vector<i64> start((size_t)L), pstart((size_t)L);
   i64 a = 0, b = 0;
   for (i64 l = 0; l < L; l++) {

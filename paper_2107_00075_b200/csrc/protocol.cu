@@ -242,8 +242,18 @@ gauss_seidel:
       L.level_mode = S.level_mode;
     }
     if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
-    if (S.level_wl && S.level_mode && S.cplan && dist == 1 && !L.old) launch_gs_cluster(*S.cplan, L.val, L.old, s);
-    else launch_gs(L, s);
+    if (S.level_wl && S.level_mode && S.cplan && dist == 1 && !L.old) {
+      launch_gs_cluster(*S.cplan, L.val, L.old, s);
+    } else {
+      if (S.level_wl && S.level_mode && S.cplan && S.cplan->chains) {
+        // a schedule with runs is for the cluster kernel only: plain id order here
+        L.wl = wl;
+        L.nwl_dev = nwl;
+        L.nwl_max = nwl_max;
+        L.level_mode = false;
+      }
+      launch_gs(L, s);
+    }
     if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
     if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
     return;
@@ -399,6 +409,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   static const bool no_fast = std::getenv("CHROMA_NO_FAST_FREE") != nullptr;
   static const bool no_levels = std::getenv("CHROMA_NO_LEVELS") != nullptr;
   static const bool no_cluster = std::getenv("CHROMA_NO_CLUSTER") != nullptr;
+  static const bool no_chains = std::getenv("CHROMA_NO_CHAINS") != nullptr;
   // round-0 schedule: 0 auto (levels if the DAG is wide, else rank-interleaved for
   // virtual ranks, else id order), 1 levels only, 2 interleave only, 3 id order
   static const int sched = (int)env_i64("CHROMA_GS_SCHEDULE", 0);
@@ -510,14 +521,18 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         // bounded degree <= 32: try the cluster kernel (gs_cluster.cu), which walks
         // narrow levels as cheaply as wide ones; otherwise only wide DAGs take levels
         const bool try_cluster = w.delta_max <= 32 && !no_cluster;
+        // the cluster kernel resolves runs of adjacent consecutive ids in one level
+        const bool chains = try_cluster && !no_chains;
         std::vector<i64> lsizes;
         w.level_mode = (sched == 0 || sched == 1) && w.delta_max <= level_max_deg &&
                        build_level_order(w.g.rowptr.p, w.g.col.p, w.NL, w.cs.wl.p, owned, w.level_wl, n, s,
-                                         &lsizes, try_cluster ? 1 : -1);
+                                         &lsizes, try_cluster ? 1 : -1, chains);
         if (w.level_mode && try_cluster &&
-            !build_cluster_plan(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, w.level_wl.p, n, lsizes, w.cplan, s)) {
-          // no cluster: keep the schedule only if it is wide enough for the dataflow kernel
-          if ((i64)lsizes.size() * 2048 > owned) w.level_mode = false;
+            !build_cluster_plan(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, w.level_wl.p, n, lsizes, w.cplan, s,
+                                chains)) {
+          // no cluster: keep the schedule only if it is wide enough for the dataflow
+          // kernel (and has no runs, which only the cluster kernel evaluates)
+          if (chains || (i64)lsizes.size() * 2048 > owned) w.level_mode = false;
         }
         w.level_n = w.level_mode ? n : 0;
         if (!w.level_mode && (sched == 0 || sched == 2) &&

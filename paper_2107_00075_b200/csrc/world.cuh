@@ -31,6 +31,7 @@ struct Csr {
 struct ClusterPlan {
   bool ok = false;
   int CL = 0, CAP = 0, DW = 0, logB = 10, logCL = 4;
+  bool chains = false;  // the schedule puts runs (gs_levels.cu) on one level
   i64 per = 0, nv = 0, L = 0;
   size_t smem = 0;
   DBuf<i32> v, nb, item_a, item_n, item_l, cta_item;
@@ -172,16 +173,19 @@ void halo_release_p2p(World& w);
 // Level schedule of a sorted worklist (padded to chunks; false if the DAG is too
 // deep and narrow to benefit).  gs_levels.cu.
 // sizes_out: the (unpadded) size of every level; min_width_override > 0 replaces the
-// minimum average level width (CHROMA_LEVEL_MIN_WIDTH, default 2048).
+// minimum average level width (CHROMA_LEVEL_MIN_WIDTH, default 2048).  chains: a
+// run of consecutive adjacent ids inside one 1024-id block shares one level (only
+// the cluster kernel, which scans runs, may consume such a schedule).
 bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl, i64 nwl, DBuf<i32>& out,
                        i64& nout, cudaStream_t s, std::vector<i64>* sizes_out = nullptr,
-                       i64 min_width_override = -1);
+                       i64 min_width_override = -1, bool chains = false);
 
 // Level-synchronous Gauss-Seidel on one thread-block cluster (gs_cluster.cu): the
 // plan is built once from a level schedule (bounded degree <= 32, colours of every
 // vertex fit the cluster's shared memory as bytes); false if not applicable.
 bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
-                        i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s);
+                        i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s,
+                        bool chains = false);
 void launch_gs_cluster(const ClusterPlan& plan, i32* val, const i32* old, cudaStream_t s);
 
 // Round-robin chunk order over the virtual ranks of a world (rank_counts = owned

@@ -302,3 +302,44 @@ def test_run_distributed_at_scale_vs_oracle(name, mode, P):
     assert [r.conflicts for r in reps] == [x["conflicts"] for x in ref_reps]
     assert [r.bytes_sent for r in reps] == [x["bytes_sent"] for x in ref_reps]
     assert [list(r.recolored_per_rank) for r in reps] == [x["recolored_per_rank"] for x in ref_reps]
+
+
+def _band_graph(n, p_chain, extra, span, seed):
+    """Bounded-degree graph with irregular runs: v ~ v-1 with probability p_chain,
+    plus `extra` random edges per vertex to v-k, k in [2, span]."""
+    rng = np.random.default_rng(seed)
+    v = np.arange(1, n)
+    keep = rng.random(n - 1) < p_chain
+    a = [v[keep]]
+    b = [v[keep] - 1]
+    for _ in range(extra):
+        x = rng.integers(span, n, size=n // 2)
+        a.append(x)
+        b.append(x - rng.integers(2, span + 1, size=x.size))
+    return G.preprocess(n, np.stack([np.concatenate(a), np.concatenate(b)], 1))
+
+
+@pytest.mark.parametrize("kind,P", [("band", 1), ("band", 4), ("band_long", 1), ("st27_60", 8), ("st27_60", 1),
+                                    ("grid1000x300", 1), ("hex40", 8)])
+def test_cluster_runs_vs_oracle(kind, P):
+    """Round 0 on the cluster kernel with runs of adjacent consecutive ids on one level
+    (map-composition prefix scan; gs_levels.cu chain mode): irregular runs, runs cut at
+    item and 1024-id block boundaries, multi-round protocols (odd slabs); colours and
+    reports equal the oracle's."""
+    g = {"band": lambda: _band_graph(300_000, 0.85, 2, 3000, 5),
+         "band_long": lambda: _band_graph(400_000, 0.98, 1, 200_000, 6),
+         "st27_60": lambda: G.gen_stencil27(60),
+         "grid1000x300": lambda: G.gen_hex_mesh(1000, 300, 1),
+         "hex40": lambda: G.gen_hex_mesh(40, 40, 40)}[kind]()
+    assert int(np.diff(g.row_offsets).max()) <= 32
+    pm = PT.partition_block(g, P)
+    mode = "d1-2gl" if P > 1 else "d1"
+    gl = R.ghost_layers_for(R.Mode(mode))
+    w = RT.build_local_graphs(g, pm, gl)
+    colors, reps = R.run_distributed(w, R.AlgorithmConfig(mode=R.Mode(mode), deterministic=True))
+    ref, ref_reps = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, gl).run(mode, False, True)
+    assert np.array_equal(colors, ref)
+    assert [r.conflicts for r in reps] == [x["conflicts"] for x in ref_reps]
+    assert [list(r.recolored_per_rank) for r in reps] == [x["recolored_per_rank"] for x in ref_reps]
+    if P == 1:
+        assert np.array_equal(colors, L.serial_greedy(g))
