@@ -92,7 +92,11 @@ __global__ void k_bounds(const u64* keys, i64 nent, i64 L, int CL, i64* bounds) 
 // in the protocol's round 0 -- worklist members below v (coloured in earlier levels)
 // and vertices outside the worklist (fixed colours); worklist members above v still
 // hold their pre-call colour, 0 on that path.
-__device__ __forceinline__ bool keep_slot(i32 u, i32 v, const uint8_t* member) { return u < v || !member[u]; }
+// zero_nm: every non-member holds colour 0 when the plan runs (the protocol's round
+// 0 before any exchange: the non-members are the ghosts), so only lower members count
+__device__ __forceinline__ bool keep_slot(i32 u, i32 v, const uint8_t* member, bool zero_nm) {
+  return zero_nm ? u < v && member[u] : u < v || !member[u];
+}
 constexpr i32 LINK = 1 << 30, PREV = 1 << 29, ID_MASK = PREV - 1;  // entry flags (run links)
 
 // level-ordered entries: is entry j's predecessor x - 1 on the same level (a run link)?
@@ -110,7 +114,7 @@ __device__ __forceinline__ bool same_level_prev(const i32* v, i64 j, const i64* 
 // widest pruned row; the x - 1 slot of a run link is not a slot (the kernel takes
 // that colour from the scan or, at an item start, from its own shared memory)
 __global__ void k_slot_count(const i64* rowptr, const i32* col, const i32* v, i64 nent, const uint8_t* member,
-                             const i64* lstart, i64 L, bool chains, unsigned* maxd) {
+                             const i64* lstart, i64 L, bool chains, bool zero_nm, unsigned* maxd) {
   unsigned m = 0;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
     const i32 x = v[j];
@@ -118,7 +122,7 @@ __global__ void k_slot_count(const i64* rowptr, const i32* col, const i32* v, i6
     unsigned d = 0;
     for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) {
       const i32 u = col[e];
-      d += keep_slot(u, x, member) && !(link && u == x - 1);
+      d += keep_slot(u, x, member, zero_nm) && !(link && u == x - 1);
     }
     m = max(m, d);
   }
@@ -136,7 +140,7 @@ __global__ void k_mark(const i32* v, i64 n, uint8_t* member) {
 // ended this CTA's previous item of the level: read from own shared memory).
 __global__ void k_fill_slots(const i64* rowptr, const i32* col, const u64* keys, const i32* ent_item,
                              const i32* item_a, const i32* item_n, i64 nent, int DW, Own own, const uint8_t* member,
-                             i32* nb, i32* v) {
+                             i32* nb, i32* v, i32* item_link, bool zero_nm) {
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
     const i32 it = ent_item[j];
     const i64 a = item_a[it], n = item_n[it];
@@ -151,10 +155,11 @@ __global__ void k_fill_slots(const i64* rowptr, const i32* col, const u64* keys,
         adj = true;
         continue;
       }
-      if (keep_slot(u, x, member)) nb[a * DW + (i64)(k++) * n + t] = own.loc(u);
+      if (keep_slot(u, x, member, zero_nm)) nb[a * DW + (i64)(k++) * n + t] = own.loc(u);
     }
     for (; k < DW; k++) nb[a * DW + (i64)k * n + t] = -1;
     v[j] = x | (adj ? (t > 0 ? LINK : PREV) : 0);
+    if (adj && t > 0) item_link[it] = 1;
   }
 }
 
@@ -183,6 +188,7 @@ struct ClusterArgs {
   const i32* item_a;    // per item: first entry
   const i32* item_n;    // per item: entries
   const i32* item_l;    // per item: level
+  const i32* item_link;  // per item: 1 if it holds LINK entries (the prefix scan runs)
   const i32* cta_item;  // [CL][L+1]: first item (global index) of level l for CTA r
   i64 L;
   i64 nv, per;  // per: bytes of colour slice per CTA
@@ -230,6 +236,7 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
       i32* snb = sv + a.CAP + 4;
       if (t == 0) cp_async4(sv + a.CAP, a.item_n + k);  // n and the level ride with the item
       if (t == 0) cp_async4(sv + a.CAP + 1, a.item_l + k);
+      if (t == 0) cp_async4(sv + a.CAP + 2, a.item_link + k);
       for (int i = t; i < n; i += blockDim.x) cp_async4(sv + i, a.v + ea + i);
       const i32* gnb = a.nb + (i64)ea * a.DW;
       const int q = n * a.DW / 4;  // n * DW is a multiple of 4 (DW is)
@@ -285,6 +292,7 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     const i32* snb = sv + a.CAP + 4;
     const i32 n = sv[a.CAP];
     const i32 lk = sv[a.CAP + 1];
+    const bool scan = sv[a.CAP + 2] != 0;
     close_levels_below(lk);  // this CTA's stores of every earlier level are out
     const bool act = t < n;
     i32 v = 0;
@@ -307,9 +315,10 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     }
     wait_level();  // every level below lk is complete everywhere
     // first fit against the gathered colours: m0, and m1 (next free) for a run link.
-    // Entry t's colour is f_t(colour of t - 1) with f_t(c) = c == p ? a : b; an
-    // unlinked entry is the constant map (p = 0, colours are >= 1).
-    int fp = 0, fa = 0, fb = 0;
+    // Entry t's colour is f_t(colour of t - 1) with f_t(c) = c == p ? a : b, packed
+    // as p | a << 8 | b << 16; an unlinked entry is the constant map (p = 0, colours
+    // are >= 1).  Composition g o f = (f.p, g(f.a), g(f.b)).
+    u32 f = 0;
     if (act) {
       int c[DW];
 #pragma unroll
@@ -322,41 +331,34 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
         const int cp = col8[a.own.offset(v - 1)];
         if (cp >= 1 && cp <= 64) m |= 1ull << (cp - 1);
       }
-      const int m0 = __ffsll((long long)~m);
-      fa = fb = m0;
-      if (linked) {
-        fp = m0;
-        fa = __ffsll((long long)(~m & ~(1ull << (m0 - 1))));
-      }
+      const u32 m0 = (u32)__ffsll((long long)~m);
+      f = m0 << 8 | m0 << 16;
+      if (linked) f = m0 | (u32)__ffsll((long long)(~m & ~(1ull << (m0 - 1)))) << 8 | m0 << 16;
     }
-    if (a.chains && __syncthreads_or(linked)) {
-      // runs: inclusive scan of map composition over the item (g o f = (f.p, g(f.a), g(f.b)))
+    auto apply = [](u32 g, u32 c) -> u32 { return c == (g & 0xffu) ? (g >> 8) & 0xffu : g >> 16; };
+    if (scan) {
+      // runs: inclusive scan of map composition over the item
       const int lane = t & 31, w = t >> 5;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int qp = __shfl_up_sync(0xffffffffu, fp, o);
-        const int qa = __shfl_up_sync(0xffffffffu, fa, o);
-        const int qb = __shfl_up_sync(0xffffffffu, fb, o);
-        if (lane >= o) {
-          const int na = qa == fp ? fa : fb, nb = qb == fp ? fa : fb;
-          fp = qp, fa = na, fb = nb;
-        }
+        const u32 q = __shfl_up_sync(0xffffffffu, f, o);
+        if (lane >= o) f = (q & 0xffu) | apply(f, (q >> 8) & 0xffu) << 8 | apply(f, q >> 16) << 16;
       }
+      if (((f >> 8) & 0xffu) == (f >> 16)) f &= ~0xffu;  // a == b: constant
       // across warps: entry 0 is unlinked, so the prefix of warps < w is a
       // constant reached from the nearest constant warp total
-      int* tot = reinterpret_cast<int*>(stages + (i64)S * stage_bytes);
-      if (lane == 31) {
-        tot[3 * w] = fp, tot[3 * w + 1] = fa, tot[3 * w + 2] = fb;
-      }
+      u32* tot = reinterpret_cast<u32*>(stages + (i64)S * stage_bytes);
+      if (lane == 31) tot[w] = f;
       __syncthreads();
-      if (w > 0 && fp != 0) {
+      if (w > 0 && (f & 0xffu) != 0) {
         int k = w - 1;
-        while (tot[3 * k] != 0) k--;
-        int cc = tot[3 * k + 2];
-        for (k++; k < w; k++) cc = cc == tot[3 * k] ? tot[3 * k + 1] : tot[3 * k + 2];
-        fb = cc == fp ? fa : fb;
+        while ((tot[k] & 0xffu) != 0) k--;
+        u32 cc = tot[k] >> 16;
+        for (k++; k < w; k++) cc = apply(tot[k], cc);
+        f = apply(f, cc) << 16;
       }
     }
+    const u32 fb = f >> 16;
     if (act) col8[a.own.offset(v)] = (unsigned char)fb;
     if (dbg) tc += clock64() - c1;
     issue(k + S - 1, nx_a, nx_n);  // into item k - 1's stage (all threads are past it)
@@ -401,7 +403,7 @@ ClusterKernel cluster_kernel(int DW) {
 // ---------------------------------------------------------------- plan
 bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
                         i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s,
-                        bool chains) {
+                        bool chains, bool zero_nm) {
   plan.ok = false;
   static const bool disabled = std::getenv("CHROMA_NO_CLUSTER") != nullptr;
   if (disabled || max_deg > 32 || nv <= 0 || level_n <= 0 || level_sizes.empty()) return false;
@@ -440,7 +442,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
     k_mark<<<grid_for(std::max<i64>(ne, 1), 256, num_sms() * 8), 256, 0, s>>>(plan.v.p, ne, member.p);
     CHROMA_REQUIRE(ne == nent, CHROMA_ERUNTIME, "cluster plan: schedule size mismatch");
     k_slot_count<<<grid_for(std::max<i64>(ne, 1), 256, num_sms() * 8), 256, 0, s>>>(
-        rowptr, col, plan.v.p, ne, member.p, ls_d.p, L, chains, maxd.p);
+        rowptr, col, plan.v.p, ne, member.p, ls_d.p, L, chains, zero_nm, maxd.p);
     count_launch(2);
   }
   unsigned hmaxd = 0;
@@ -451,7 +453,9 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   i64 per = 0;
   const int logB = 10;
   const i64 nblocks = (nv + (1ll << logB) - 1) >> logB;
+  static const int cl_env = std::getenv("CHROMA_CLUSTER_SIZE") ? std::atoi(std::getenv("CHROMA_CLUSTER_SIZE")) : 0;
   for (int cl : {16, 8}) {
+    if (cl_env && cl != cl_env) continue;
     per = (nblocks + cl - 1) / cl << logB;  // colour bytes per CTA (whole blocks)
     const i64 per_pad = (per + 15) / 16 * 16;
     const i64 room = (i64)max_smem - per_pad - 16 - 1024 - 32 * 12;
@@ -523,6 +527,8 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   plan.item_a.upload(ia.data(), std::max<i64>(nitems, 1), s);
   plan.item_n.upload(in.data(), std::max<i64>(nitems, 1), s);
   plan.item_l.upload(il.data(), std::max<i64>(nitems, 1), s);
+  plan.item_link.alloc(std::max<i64>(nitems, 1), s);
+  plan.item_link.zero(s);
   plan.cta_item.upload(ci.data(), (i64)ci.size(), s);
   DBuf<i32> ent_item;
   ent_item.alloc(std::max<i64>(nent, 1), s);
@@ -530,11 +536,13 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
       plan.item_a.p, plan.item_n.p, nitems, ent_item.p);
   plan.nb.alloc(std::max<i64>(nent * DW, 1), s);
   k_fill_slots<<<grid_for(std::max<i64>(nent, 1), 256, num_sms() * 8), 256, 0, s>>>(
-      rowptr, col, keys.p, ent_item.p, plan.item_a.p, plan.item_n.p, nent, DW, own, member.p, plan.nb.p, plan.v.p);
+      rowptr, col, keys.p, ent_item.p, plan.item_a.p, plan.item_n.p, nent, DW, own, member.p, plan.nb.p, plan.v.p,
+      plan.item_link.p, zero_nm);
   count_launch(2);
   CUDA_CHECK(cudaStreamSynchronize(s));
   plan.CL = CL;
   plan.chains = chains;
+  plan.zero_nm = zero_nm;
   plan.CAP = CAP;
   plan.DW = DW;
   plan.per = per;
@@ -575,6 +583,7 @@ void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStrea
   a.item_a = p.item_a.p;
   a.item_n = p.item_n.p;
   a.item_l = p.item_l.p;
+  a.item_link = p.item_link.p;
   a.cta_item = p.cta_item.p;
   a.L = p.L;
   a.nv = p.nv;

@@ -529,7 +529,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
                                          &lsizes, try_cluster ? 1 : -1, chains);
         if (w.level_mode && try_cluster &&
             !build_cluster_plan(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, w.level_wl.p, n, lsizes, w.cplan, s,
-                                chains)) {
+                                chains, !hubs_done)) {
           // no cluster: keep the schedule only if it is wide enough for the dataflow
           // kernel (and has no runs, which only the cluster kernel evaluates)
           if (chains || (i64)lsizes.size() * 2048 > owned) w.level_mode = false;
@@ -545,7 +545,8 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         w.cs.level_wl = w.level_wl.p;
         w.cs.level_n = w.level_n;
         w.cs.level_mode = w.level_mode;
-        w.cs.cplan = w.level_mode && w.cplan.ok ? &w.cplan : nullptr;
+        // a plan without ghost slots needs every ghost at 0 (no pre-coloured hubs)
+        w.cs.cplan = w.level_mode && w.cplan.ok && !(w.cplan.zero_nm && hubs_done) ? &w.cplan : nullptr;
       }
     }
     rt_mark("hubs+worklist");

@@ -32,9 +32,10 @@ struct ClusterPlan {
   bool ok = false;
   int CL = 0, CAP = 0, DW = 0, logB = 10, logCL = 4;
   bool chains = false;  // the schedule puts runs (gs_levels.cu) on one level
+  bool zero_nm = false;  // built assuming every non-member colour is 0 (slots dropped)
   i64 per = 0, nv = 0, L = 0;
   size_t smem = 0;
-  DBuf<i32> v, nb, item_a, item_n, item_l, cta_item;
+  DBuf<i32> v, nb, item_a, item_n, item_l, item_link, cta_item;
 };
 
 // Colouring scratch shared by every entry point that colours a CSR.
@@ -185,7 +186,7 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
 // vertex fit the cluster's shared memory as bytes); false if not applicable.
 bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
                         i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s,
-                        bool chains = false);
+                        bool chains = false, bool zero_nonmembers = false);
 void launch_gs_cluster(const ClusterPlan& plan, i32* val, const i32* old, cudaStream_t s);
 
 // Round-robin chunk order over the virtual ranks of a world (rank_counts = owned
