@@ -140,7 +140,7 @@ __global__ void k_mark(const i32* v, i64 n, uint8_t* member) {
 // ended this CTA's previous item of the level: read from own shared memory).
 __global__ void k_fill_slots(const i64* rowptr, const i32* col, const u64* keys, const i32* ent_item,
                              const i32* item_a, const i32* item_n, i64 nent, int DW, Own own, const uint8_t* member,
-                             i32* nb, i32* v, i32* item_link, bool zero_nm) {
+                             i32* nb, i32* v, i32* item_link, bool zero_nm, i32 empty_off) {
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
     const i32 it = ent_item[j];
     const i64 a = item_a[it], n = item_n[it];
@@ -157,7 +157,9 @@ __global__ void k_fill_slots(const i64* rowptr, const i32* col, const u64* keys,
       }
       if (keep_slot(u, x, member, zero_nm)) nb[a * DW + (i64)(k++) * n + t] = own.loc(u);
     }
-    for (; k < DW; k++) nb[a * DW + (i64)k * n + t] = -1;
+    // empty slots: the zero byte past this CTA's colour slice
+    const i32 empty = (i32)((u32)own.owner(x) << 24) | empty_off;
+    for (; k < DW; k++) nb[a * DW + (i64)k * n + t] = empty;
     v[j] = x | (adj ? (t > 0 ? LINK : PREV) : 0);
     if (adj && t > 0) item_link[it] = 1;
   }
@@ -175,6 +177,11 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* g) {
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(g) : "memory");
+}
+__device__ __forceinline__ u32 shl1(u32 c) {
+  u32 r;
+  asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(c));
+  return r;
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -297,8 +304,8 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     const bool act = t < n;
     i32 v = 0;
     bool linked = false, prev = false;  // run link: x - 1 is the previous entry (LINK, PREV)
-    // every slot's byte address in the cluster's shared window (mapa); empty slots
-    // read a zero byte of this CTA
+    // every slot's byte address in the cluster's shared window (mapa); slots hold
+    // owner << 24 | offset, empty ones point at a zero byte of this CTA
     u32 ad[DW];
     if (act) {
       v = sv[t];
@@ -307,10 +314,8 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
       v &= ID_MASK;
 #pragma unroll
       for (int j = 0; j < DW; j++) {
-        const i32 x = snb[j * n + t];
-        const u32 q = x >= 0 ? (u32)x >> 24 : (u32)r;
-        const u32 off = x >= 0 ? (u32)x & 0xffffffu : (u32)per_pad;
-        asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ad[j]) : "r"(base8 + off), "r"(q));
+        const u32 x = (u32)snb[j * n + t];
+        asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ad[j]) : "r"(base8 + (x & 0xffffffu)), "r"(x >> 24));
       }
     }
     wait_level();  // every level below lk is complete everywhere
@@ -323,17 +328,30 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
       int c[DW];
 #pragma unroll
       for (int j = 0; j < DW; j++) asm volatile("ld.shared::cluster.u8 %0, [%1];" : "=r"(c[j]) : "r"(ad[j]));
-      u64 m = 0;
+      u32 m0, m1;
+      if (DW <= 28) {
+        // first fit of <= DW + 1 neighbours (+ x - 1) is <= 31: a 32-bit mask with
+        // bit c for colour c (bit 0 preset); PTX shl clamps, colours >= 32 drop out
+        u32 m = 1;
 #pragma unroll
-      for (int j = 0; j < DW; j++)
-        if (c[j] >= 1 && c[j] <= 64) m |= 1ull << (c[j] - 1);
-      if (prev) {
-        const int cp = col8[a.own.offset(v - 1)];
-        if (cp >= 1 && cp <= 64) m |= 1ull << (cp - 1);
+        for (int j = 0; j < DW; j++) m |= shl1(c[j]);
+        if (prev) m |= shl1(col8[a.own.offset(v - 1)]);
+        m0 = (u32)__ffs(~m) - 1;
+        m1 = (u32)__ffs(~m & ~(1u << m0)) - 1;
+      } else {
+        u64 m = 0;
+#pragma unroll
+        for (int j = 0; j < DW; j++)
+          if (c[j] >= 1 && c[j] <= 64) m |= 1ull << (c[j] - 1);
+        if (prev) {
+          const int cp = col8[a.own.offset(v - 1)];
+          if (cp >= 1 && cp <= 64) m |= 1ull << (cp - 1);
+        }
+        m0 = (u32)__ffsll((long long)~m);
+        m1 = (u32)__ffsll((long long)(~m & ~(1ull << (m0 - 1))));
       }
-      const u32 m0 = (u32)__ffsll((long long)~m);
       f = m0 << 8 | m0 << 16;
-      if (linked) f = m0 | (u32)__ffsll((long long)(~m & ~(1ull << (m0 - 1)))) << 8 | m0 << 16;
+      if (linked) f = m0 | m1 << 8 | m0 << 16;
     }
     auto apply = [](u32 g, u32 c) -> u32 { return c == (g & 0xffu) ? (g >> 8) & 0xffu : g >> 16; };
     if (scan) {
@@ -524,6 +542,10 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
     }
   if (nent >= (1ll << 31) || (i64)ia.size() >= (1ll << 31)) return false;
   const i64 nitems = (i64)ia.size();
+  // launch only the threads the largest item needs (whole warps)
+  i32 maxn = 32;
+  for (i32 x : in) maxn = std::max(maxn, x);
+  plan.nthreads = (maxn + 31) / 32 * 32;
   plan.item_a.upload(ia.data(), std::max<i64>(nitems, 1), s);
   plan.item_n.upload(in.data(), std::max<i64>(nitems, 1), s);
   plan.item_l.upload(il.data(), std::max<i64>(nitems, 1), s);
@@ -537,7 +559,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   plan.nb.alloc(std::max<i64>(nent * DW, 1), s);
   k_fill_slots<<<grid_for(std::max<i64>(nent, 1), 256, num_sms() * 8), 256, 0, s>>>(
       rowptr, col, keys.p, ent_item.p, plan.item_a.p, plan.item_n.p, nent, DW, own, member.p, plan.nb.p, plan.v.p,
-      plan.item_link.p, zero_nm);
+      plan.item_link.p, zero_nm, (i32)((per + 15) / 16 * 16));
   count_launch(2);
   CUDA_CHECK(cudaStreamSynchronize(s));
   plan.CL = CL;
@@ -571,8 +593,8 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   }
   static const bool trace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
   if (trace)
-    std::fprintf(stderr, "[cluster] %d CTAs x %d threads, %lld levels, %lld entries, %lld items, DW %d, smem %zu%s\n",
-                 CL, CAP, (long long)L, (long long)nent, (long long)nitems, DW, plan.smem, chains ? ", runs" : "");
+    std::fprintf(stderr, "[cluster] %d CTAs x %d (cap %d) threads, %lld levels, %lld entries, %lld items, DW %d, smem %zu%s\n",
+                 CL, plan.nthreads, CAP, (long long)L, (long long)nent, (long long)nitems, DW, plan.smem, chains ? ", runs" : "");
   return true;
 }
 
@@ -612,7 +634,7 @@ void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStrea
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(p.CL);
-  cfg.blockDim = dim3((unsigned)p.CAP);
+  cfg.blockDim = dim3((unsigned)(p.nthreads > 0 ? p.nthreads : p.CAP));
   cfg.dynamicSmemBytes = p.smem;
   cfg.stream = s;
   cfg.attrs = attr;

@@ -30,7 +30,7 @@ struct Csr {
 // Level-synchronous Gauss-Seidel plan for one thread-block cluster (gs_cluster.cu)
 struct ClusterPlan {
   bool ok = false;
-  int CL = 0, CAP = 0, DW = 0, logB = 10, logCL = 4;
+  int CL = 0, CAP = 0, DW = 0, logB = 10, logCL = 4, nthreads = 0;
   bool chains = false;  // the schedule puts runs (gs_levels.cu) on one level
   bool zero_nm = false;  // built assuming every non-member colour is 0 (slots dropped)
   i64 per = 0, nv = 0, L = 0;
