@@ -139,12 +139,14 @@ __global__ void k_mark(const i32* v, i64 n, uint8_t* member) {
 // previous entry of this item: the prefix scan supplies its colour) or PREV (x - 1
 // ended this CTA's previous item of the level: read from own shared memory).
 __global__ void k_fill_slots(const i64* rowptr, const i32* col, const u64* keys, const i32* ent_item,
-                             const i32* item_a, const i32* item_n, i64 nent, int DW, Own own, const uint8_t* member,
-                             i32* nb, i32* v, i32* item_link, bool zero_nm, i32 empty_off) {
+                             const i32* item_a, const i32* item_n, const i64* item_o, i64 nent, int DW, Own own,
+                             const uint8_t* member, i32* blob, bool zero_nm, i32 empty_off) {
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < nent; j += (i64)gridDim.x * blockDim.x) {
     const i32 it = ent_item[j];
-    const i64 a = item_a[it], n = item_n[it];
+    const i64 a = item_a[it], n = (item_n[it] + 3) & ~3;  // n: the padded row length
     const i64 t = j - a;
+    i32* hdr = blob + item_o[it];
+    i32* nb = hdr + 4 + n;  // slot k of entry t at nb[k * n + t]
     const i32 x = (i32)(keys[j] & 0xffffffffu);
     const bool cand = j > 0 && (keys[j - 1] >> 36) == (keys[j] >> 36) && (i32)(keys[j - 1] & 0xffffffffu) == x - 1;
     bool adj = false;
@@ -155,13 +157,23 @@ __global__ void k_fill_slots(const i64* rowptr, const i32* col, const u64* keys,
         adj = true;
         continue;
       }
-      if (keep_slot(u, x, member, zero_nm)) nb[a * DW + (i64)(k++) * n + t] = own.loc(u);
+      if (keep_slot(u, x, member, zero_nm)) nb[(i64)(k++) * n + t] = own.loc(u);
     }
     // empty slots: the zero byte past this CTA's colour slice
     const i32 empty = (i32)((u32)own.owner(x) << 24) | empty_off;
-    for (; k < DW; k++) nb[a * DW + (i64)k * n + t] = empty;
-    v[j] = x | (adj ? (t > 0 ? LINK : PREV) : 0);
-    if (adj && t > 0) item_link[it] = 1;
+    for (; k < DW; k++) nb[(i64)k * n + t] = empty;
+    hdr[4 + t] = x | (adj ? (t > 0 ? LINK : PREV) : 0);
+    if (adj && t > 0) hdr[2] = 1;
+  }
+}
+
+__global__ void k_item_hdr(const i32* item_n, const i32* item_l, const i64* item_o, i64 nitems, i32* blob) {
+  for (i64 it = blockIdx.x * (i64)blockDim.x + threadIdx.x; it < nitems; it += (i64)gridDim.x * blockDim.x) {
+    i32* h = blob + item_o[it];
+    h[0] = item_n[it];
+    h[1] = item_l[it];
+    h[2] = 0;
+    h[3] = (item_n[it] + 3) & ~3;
   }
 }
 
@@ -190,12 +202,9 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 struct ClusterArgs {
-  const i32* v;         // entries
-  const i32* nb;        // transposed slots
-  const i32* item_a;    // per item: first entry
-  const i32* item_n;    // per item: entries
-  const i32* item_l;    // per item: level
-  const i32* item_link;  // per item: 1 if it holds LINK entries (the prefix scan runs)
+  const i32* blob;      // items: [n, level, link, npad | ids x npad | slots DW x npad]
+  const i64* item_o;    // per item: offset in blob (ints, multiple of 4)
+  const i32* item_sz;   // per item: size (ints, multiple of 4)
   const i32* cta_item;  // [CL][L+1]: first item (global index) of level l for CTA r
   i64 L;
   i64 nv, per;  // per: bytes of colour slice per CTA
@@ -217,10 +226,16 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
   const int t = threadIdx.x;
   const i64 per_pad = (a.per + 15) / 16 * 16;
   unsigned char* col8 = smem;
-  const i64 stage_bytes = ((i64)a.CAP * (a.DW + 1) + 4) * 4;  // [v x CAP | n, pad x3 | slots]
+  const i64 stage_bytes = ((i64)a.CAP * (a.DW + 1) + 4) * 4;  // one item: header, ids, slots
   unsigned char* stages = smem + per_pad + 16;
+  const u32 mbar = (u32)__cvta_generic_to_shared(stages + (i64)S * stage_bytes);  // S mbarriers
+  u32* tot = reinterpret_cast<u32*>(stages + (i64)S * stage_bytes + 32);         // scan: warp totals
   const u32 base8 = (u32)__cvta_generic_to_shared(col8);
-  if (t == 0) col8[per_pad] = 0;  // the byte empty slots read
+  if (t == 0) {
+    col8[per_pad] = 0;  // the byte empty slots read
+    for (int q = 0; q < S; q++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar + 8 * q) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   // ---- my colour slice: pre-call colours (worklist entries: their old colour)
   const int lB = a.own.logB, lC = a.own.logCL;
   for (i64 o = t; o < a.per; o += blockDim.x) {
@@ -234,29 +249,33 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
   }
   const i32* my_item = a.cta_item + (i64)r * (a.L + 1);
   const i32 k_begin = my_item[0], k_end = my_item[a.L];
-  // item descriptors are read one item ahead of their cp.async issue (the global
-  // load stays off the per-level chain)
-  auto issue = [&](i32 k, i32 ea, i32 n) {
-    if (k < k_end) {
-      unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
-      i32* sv = reinterpret_cast<i32*>(st);
-      i32* snb = sv + a.CAP + 4;
-      if (t == 0) cp_async4(sv + a.CAP, a.item_n + k);  // n and the level ride with the item
-      if (t == 0) cp_async4(sv + a.CAP + 1, a.item_l + k);
-      if (t == 0) cp_async4(sv + a.CAP + 2, a.item_link + k);
-      for (int i = t; i < n; i += blockDim.x) cp_async4(sv + i, a.v + ea + i);
-      const i32* gnb = a.nb + (i64)ea * a.DW;
-      const int q = n * a.DW / 4;  // n * DW is a multiple of 4 (DW is)
-      for (int i = t; i < q; i += blockDim.x) cp_async16(snb + 4 * i, gnb + 4 * i);
+  // items stream in by TMA bulk copies (one instruction per item, issued by thread
+  // 0, completion on the stage's mbarrier), S - 1 items ahead; thread 0 reads the
+  // next descriptor one item ahead of its issue (off the per-level chain)
+  auto issue = [&](i32 k, i64 off, i32 sz) {
+    if (t == 0 && k < k_end) {
+      const int q = (k - k_begin) % S;
+      const u32 dst = (u32)__cvta_generic_to_shared(stages + (i64)q * stage_bytes);
+      const u32 bytes = (u32)sz * 4u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar + 8 * q), "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "l"(a.blob + off), "r"(bytes), "r"(mbar + 8 * q)
+          : "memory");
     }
-    cp_commit();
   };
+  __syncthreads();  // barriers initialised
   for (int k = 0; k < S - 1; k++) {
     const i32 kk = k_begin + k;
-    issue(kk, kk < k_end ? a.item_a[kk] : 0, kk < k_end ? a.item_n[kk] : 0);
+    if (t == 0 && kk < k_end) issue(kk, a.item_o[kk], a.item_sz[kk]);
   }
-  i32 nx_a = k_begin + S - 1 < k_end ? a.item_a[k_begin + S - 1] : 0;
-  i32 nx_n = k_begin + S - 1 < k_end ? a.item_n[k_begin + S - 1] : 0;
+  i64 nx_o = 0;
+  i32 nx_sz = 0;
+  if (t == 0 && k_begin + S - 1 < k_end) {
+    nx_o = a.item_o[k_begin + S - 1];
+    nx_sz = a.item_sz[k_begin + S - 1];
+  }
   cluster.sync();
   long long tw = 0, tc = 0, ts = 0, ni = 0;
   const bool dbg = a.dbg && r == 0 && t == 0;
@@ -290,16 +309,28 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
   };
   for (i32 k = k_begin; k < k_end; k++) {
     const long long c0 = dbg ? clock64() : 0;
-    cp_wait<S - 2>();
+    {
+      const int q = (k - k_begin) % S;
+      const u32 par = (u32)((k - k_begin) / S) & 1u;
+      asm volatile(
+          "{\n\t.reg .pred p;\n"
+          "WAIT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra WAIT_%=;\n}" ::"r"(mbar + 8 * q),
+          "r"(par)
+          : "memory");
+    }
     __syncthreads();  // stage k landed; every thread is past item k - 1
     const long long c1 = dbg ? clock64() : 0;
     if (dbg) tw += c1 - c0, ni++;
     const unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
-    const i32* sv = reinterpret_cast<const i32*>(st);
-    const i32* snb = sv + a.CAP + 4;
-    const i32 n = sv[a.CAP];
-    const i32 lk = sv[a.CAP + 1];
-    const bool scan = sv[a.CAP + 2] != 0;
+    const i32* sh = reinterpret_cast<const i32*>(st);
+    const i32 n = sh[0];
+    const i32 lk = sh[1];
+    const bool scan = sh[2] != 0;
+    const i32 npad = sh[3];
+    const i32* sv = sh + 4;
+    const i32* snb = sv + npad;
     close_levels_below(lk);  // this CTA's stores of every earlier level are out
     const bool act = t < n;
     i32 v = 0;
@@ -314,7 +345,7 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
       v &= ID_MASK;
 #pragma unroll
       for (int j = 0; j < DW; j++) {
-        const u32 x = (u32)snb[j * n + t];
+        const u32 x = (u32)snb[j * npad + t];
         asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ad[j]) : "r"(base8 + (x & 0xffffffu)), "r"(x >> 24));
       }
     }
@@ -365,7 +396,6 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
       if (((f >> 8) & 0xffu) == (f >> 16)) f &= ~0xffu;  // a == b: constant
       // across warps: entry 0 is unlinked, so the prefix of warps < w is a
       // constant reached from the nearest constant warp total
-      u32* tot = reinterpret_cast<u32*>(stages + (i64)S * stage_bytes);
       if (lane == 31) tot[w] = f;
       __syncthreads();
       if (w > 0 && (f & 0xffu) != 0) {
@@ -379,15 +409,16 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     const u32 fb = f >> 16;
     if (act) col8[a.own.offset(v)] = (unsigned char)fb;
     if (dbg) tc += clock64() - c1;
-    issue(k + S - 1, nx_a, nx_n);  // into item k - 1's stage (all threads are past it)
-    if (k + S < k_end) {
-      nx_a = a.item_a[k + S];
-      nx_n = a.item_n[k + S];
+    if (t == 0) {
+      issue(k + S - 1, nx_o, nx_sz);  // into item k - 1's stage (all threads are past it)
+      if (k + S < k_end) {
+        nx_o = a.item_o[k + S];
+        nx_sz = a.item_sz[k + S];
+      }
     }
   }
   close_levels_below(a.L);
   wait_level();
-  cp_wait<0>();
   // colours back to global memory once, at the end (no global stores inside the
   // level loop for the cluster barriers to drain): worklist entries still read PENDING
   for (i64 o = t; o < a.per; o += blockDim.x) {
@@ -546,22 +577,36 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   i32 maxn = 32;
   for (i32 x : in) maxn = std::max(maxn, x);
   plan.nthreads = (maxn + 31) / 32 * 32;
-  plan.item_a.upload(ia.data(), std::max<i64>(nitems, 1), s);
-  plan.item_n.upload(in.data(), std::max<i64>(nitems, 1), s);
-  plan.item_l.upload(il.data(), std::max<i64>(nitems, 1), s);
-  plan.item_link.alloc(std::max<i64>(nitems, 1), s);
-  plan.item_link.zero(s);
+  // blob: per item [n, level, link, npad | ids | slots], rows padded to npad = n
+  // rounded up to 4, so every item is a whole number of 16-byte units (TMA bulk copy)
+  std::vector<i64> io((size_t)nitems);
+  std::vector<i32> isz((size_t)nitems);
+  i64 total = 0;
+  for (i64 it = 0; it < nitems; it++) {
+    io[(size_t)it] = total;
+    isz[(size_t)it] = 4 + (in[(size_t)it] + 3) / 4 * 4 * (DW + 1);
+    total += isz[(size_t)it];
+  }
+  DBuf<i32> item_a, item_n, item_l;
+  item_a.upload(ia.data(), std::max<i64>(nitems, 1), s);
+  item_n.upload(in.data(), std::max<i64>(nitems, 1), s);
+  item_l.upload(il.data(), std::max<i64>(nitems, 1), s);
+  plan.item_o.upload(io.data(), std::max<i64>(nitems, 1), s);
+  plan.item_sz.upload(isz.data(), std::max<i64>(nitems, 1), s);
   plan.cta_item.upload(ci.data(), (i64)ci.size(), s);
+  plan.blob.alloc(std::max<i64>(total, 4), s);
+  k_item_hdr<<<grid_for(std::max<i64>(nitems, 1), 256, num_sms() * 8), 256, 0, s>>>(item_n.p, item_l.p,
+                                                                                    plan.item_o.p, nitems, plan.blob.p);
   DBuf<i32> ent_item;
   ent_item.alloc(std::max<i64>(nent, 1), s);
   k_ent_item<<<(int)std::min<i64>(std::max<i64>(nitems, 1), (i64)num_sms() * 16), 256, 0, s>>>(
-      plan.item_a.p, plan.item_n.p, nitems, ent_item.p);
-  plan.nb.alloc(std::max<i64>(nent * DW, 1), s);
+      item_a.p, item_n.p, nitems, ent_item.p);
   k_fill_slots<<<grid_for(std::max<i64>(nent, 1), 256, num_sms() * 8), 256, 0, s>>>(
-      rowptr, col, keys.p, ent_item.p, plan.item_a.p, plan.item_n.p, nent, DW, own, member.p, plan.nb.p, plan.v.p,
-      plan.item_link.p, zero_nm, (i32)((per + 15) / 16 * 16));
-  count_launch(2);
+      rowptr, col, keys.p, ent_item.p, item_a.p, item_n.p, plan.item_o.p, nent, DW, own, member.p, plan.blob.p,
+      zero_nm, (i32)((per + 15) / 16 * 16));
+  count_launch(3);
   CUDA_CHECK(cudaStreamSynchronize(s));
+  plan.v.release();
   plan.CL = CL;
   plan.chains = chains;
   plan.zero_nm = zero_nm;
@@ -574,23 +619,6 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   plan.L = L;
   plan.smem = (size_t)((per + 15) / 16 * 16 + 16 + (i64)S * ((i64)CAP * (DW + 1) + 4) * 4 + 32 * 12);
   plan.ok = true;
-  if (const char* dump = std::getenv("CHROMA_CLUSTER_DUMP")) {
-    // dev aid: the plan as raw arrays (n_ent v, n_items a, n, CL*(L+1) cta_item, nent*DW slots)
-    std::vector<i32> hv((size_t)nent), hnb((size_t)(nent * DW));
-    CUDA_CHECK(cudaMemcpy(hv.data(), plan.v.p, sizeof(i32) * nent, cudaMemcpyDeviceToHost));
-    CUDA_CHECK(cudaMemcpy(hnb.data(), plan.nb.p, sizeof(i32) * nent * DW, cudaMemcpyDeviceToHost));
-    if (FILE* fh = std::fopen(dump, "wb")) {
-      const i64 hdr[6] = {nent, nitems, (i64)CL, L, (i64)DW, per};
-      std::fwrite(hdr, sizeof(hdr), 1, fh);
-      std::fwrite(hv.data(), 4, hv.size(), fh);
-      std::fwrite(ia.data(), 4, ia.size(), fh);
-      std::fwrite(in.data(), 4, in.size(), fh);
-      std::fwrite(ci.data(), 4, ci.size(), fh);
-      std::fwrite(hnb.data(), 4, hnb.size(), fh);
-      std::fwrite(lstart.data(), 8, lstart.size(), fh);
-      std::fclose(fh);
-    }
-  }
   static const bool trace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
   if (trace)
     std::fprintf(stderr, "[cluster] %d CTAs x %d (cap %d) threads, %lld levels, %lld entries, %lld items, DW %d, smem %zu%s\n",
@@ -600,12 +628,9 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
 
 void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStream_t s) {
   ClusterArgs a;
-  a.v = p.v.p;
-  a.nb = p.nb.p;
-  a.item_a = p.item_a.p;
-  a.item_n = p.item_n.p;
-  a.item_l = p.item_l.p;
-  a.item_link = p.item_link.p;
+  a.blob = p.blob.p;
+  a.item_o = p.item_o.p;
+  a.item_sz = p.item_sz.p;
   a.cta_item = p.cta_item.p;
   a.L = p.L;
   a.nv = p.nv;

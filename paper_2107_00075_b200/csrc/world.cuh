@@ -35,7 +35,8 @@ struct ClusterPlan {
   bool zero_nm = false;  // built assuming every non-member colour is 0 (slots dropped)
   i64 per = 0, nv = 0, L = 0;
   size_t smem = 0;
-  DBuf<i32> v, nb, item_a, item_n, item_l, item_link, cta_item;
+  DBuf<i32> v, blob, item_sz, cta_item;  // v: scratch of the plan build
+  DBuf<i64> item_o;
 };
 
 // Colouring scratch shared by every entry point that colours a CSR.
