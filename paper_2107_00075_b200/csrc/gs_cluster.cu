@@ -214,7 +214,7 @@ struct ClusterArgs {
   i32* val;
   const i32* old;
   int exp;                  // dev experiments (timing only): 1 no remote loads, 2 no global store, 4 item_n from smem
-  unsigned long long* dbg;  // optional [4] clock sums of CTA 0 (wait, colour, cluster sync, items)
+  unsigned long long* dbg;  // optional [8] clocks of CTA 0 (wait, colour, cluster sync, items, start, loop, end, issue)
 };
 
 template <int DW>
@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
   const int t = threadIdx.x;
   const i64 per_pad = (a.per + 15) / 16 * 16;
   unsigned char* col8 = smem;
+  const long long t_start = clock64();
   const i64 stage_bytes = ((i64)a.CAP * (a.DW + 1) + 4) * 4;  // one item: header, ids, slots
   unsigned char* stages = smem + per_pad + 16;
   const u32 mbar = (u32)__cvta_generic_to_shared(stages + (i64)S * stage_bytes);  // S mbarriers
@@ -238,14 +239,26 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
   }
   // ---- my colour slice: pre-call colours (worklist entries: their old colour)
   const int lB = a.own.logB, lC = a.own.logCL;
-  for (i64 o = t; o < a.per; o += blockDim.x) {
+  // four ids per thread and step (16-byte loads; a block of 2^lB ids is contiguous)
+  auto pre = [&](i64 x) -> u32 {
+    if (x >= a.nv) return 0;
+    i32 c = a.val[x];
+    if (c == PENDING) c = a.old ? a.old[x] : 0;
+    return (c < 0 || c > 255) ? 0u : (u32)c;
+  };
+#pragma unroll 4
+  for (i64 u = t; u < a.per / 4; u += blockDim.x) {
+    const i64 o = 4 * u;
     const i64 x = ((((o >> lB) << lC) + r) << lB) | (o & ((1ll << lB) - 1));
-    i32 c = 0;
-    if (x < a.nv) {
-      c = a.val[x];
-      if (c == PENDING) c = a.old ? a.old[x] : 0;
+    u32 w4;
+    if (x + 3 < a.nv && !a.old) {
+      const int4 c = *reinterpret_cast<const int4*>(a.val + x);
+      auto b = [](i32 c) -> u32 { return (c == PENDING || c < 0 || c > 255) ? 0u : (u32)c; };
+      w4 = b(c.x) | b(c.y) << 8 | b(c.z) << 16 | b(c.w) << 24;
+    } else {
+      w4 = pre(x) | pre(x + 1) << 8 | pre(x + 2) << 16 | pre(x + 3) << 24;
     }
-    col8[o] = (unsigned char)((c < 0 || c > 255) ? 0 : c);
+    *reinterpret_cast<u32*>(col8 + o) = w4;
   }
   const i32* my_item = a.cta_item + (i64)r * (a.L + 1);
   const i32 k_begin = my_item[0], k_end = my_item[a.L];
@@ -277,7 +290,8 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     nx_sz = a.item_sz[k_begin + S - 1];
   }
   cluster.sync();
-  long long tw = 0, tc = 0, ts = 0, ni = 0;
+  long long tw = 0, tc = 0, ts = 0, ni = 0, ti = 0;
+  const long long t_loop = clock64();
   const bool dbg = a.dbg && r == 0 && t == 0;
   // Level barriers, split and item-driven.  Every CTA passes L barriers (one per
   // level), in order; it arrives at level l's barrier once its stores of level l are
@@ -409,6 +423,7 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     const u32 fb = f >> 16;
     if (act) col8[a.own.offset(v)] = (unsigned char)fb;
     if (dbg) tc += clock64() - c1;
+    const long long c3 = dbg ? clock64() : 0;
     if (t == 0) {
       issue(k + S - 1, nx_o, nx_sz);  // into item k - 1's stage (all threads are past it)
       if (k + S < k_end) {
@@ -416,20 +431,39 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
         nx_sz = a.item_sz[k + S];
       }
     }
+    if (dbg) ti += clock64() - c3;
   }
+  const long long t_end = clock64();
   close_levels_below(a.L);
   wait_level();
   // colours back to global memory once, at the end (no global stores inside the
   // level loop for the cluster barriers to drain): worklist entries still read PENDING
-  for (i64 o = t; o < a.per; o += blockDim.x) {
+#pragma unroll 4
+  for (i64 u = t; u < a.per / 4; u += blockDim.x) {
+    const i64 o = 4 * u;
     const i64 x = ((((o >> lB) << lC) + r) << lB) | (o & ((1ll << lB) - 1));
-    if (x < a.nv && a.val[x] == PENDING) a.val[x] = col8[o];
+    const u32 w4 = *reinterpret_cast<const u32*>(col8 + o);
+    if (x + 3 < a.nv) {
+      int4 c = *reinterpret_cast<const int4*>(a.val + x);
+      c.x = c.x == PENDING ? (i32)(w4 & 0xffu) : c.x;
+      c.y = c.y == PENDING ? (i32)((w4 >> 8) & 0xffu) : c.y;
+      c.z = c.z == PENDING ? (i32)((w4 >> 16) & 0xffu) : c.z;
+      c.w = c.w == PENDING ? (i32)(w4 >> 24) : c.w;
+      *reinterpret_cast<int4*>(a.val + x) = c;
+    } else {
+      for (int i = 0; i < 4; i++)
+        if (x + i < a.nv && a.val[x + i] == PENDING) a.val[x + i] = (i32)((w4 >> (8 * i)) & 0xffu);
+    }
   }
   if (dbg) {
     a.dbg[0] = tw;
     a.dbg[1] = tc;
     a.dbg[2] = ts;
     a.dbg[3] = ni;
+    a.dbg[4] = t_loop - t_start;
+    a.dbg[5] = t_end - t_loop;
+    a.dbg[6] = clock64() - t_end;
+    a.dbg[7] = ti;
   }
 }
 
@@ -648,7 +682,7 @@ void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStrea
   DBuf<unsigned long long> dbg;
   a.dbg = nullptr;
   if (trace) {
-    dbg.alloc(4, s);
+    dbg.alloc(8, s);
     dbg.zero(s);
     a.dbg = dbg.p;
   }
@@ -668,11 +702,13 @@ void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStrea
   count_launch();
   CUDA_CHECK(cudaGetLastError());
   if (trace) {
-    unsigned long long h[4];
+    unsigned long long h[8];
     CUDA_CHECK(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-    std::fprintf(stderr, "[cluster] CTA0 cycles: wait %llu colour %llu cluster-sync %llu over %llu items, %lld levels\n",
-                 h[0], h[1], h[2], h[3], (long long)p.L);
+    std::fprintf(stderr,
+                 "[cluster] CTA0 cycles: wait %llu colour %llu cluster-sync %llu issue %llu over %llu items, %lld "
+                 "levels; start %llu loop %llu end %llu\n",
+                 h[0], h[1], h[2], h[7], h[3], (long long)p.L, h[4], h[5], h[6]);
   }
 }
 
