@@ -61,6 +61,13 @@ __global__ void k_count_recolored(const i32* wl, const i64* nwl, const uint8_t* 
     }
     run++;
   }
+  // last run: one shared atomic per warp and rank (lanes mostly share one rank)
+  {
+    const unsigned grp = __match_any_sync(0xffffffffu, cur);
+    const unsigned tot = __reduce_add_sync(grp, (unsigned)run);
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1)) run = tot;
+    else run = 0;
+  }
   flush();
   __syncthreads();
   if (local_hist)
@@ -502,7 +509,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
       select_flagged(w.cs.flags.p, w.NL, w.cs.wl.p, w.cs.nwl.p, s);
       nwl_host = w.NL;
     }
-    k_count_recolored<<<G(w.NL), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
+    k_count_recolored<<<std::min(G(w.NL), num_sms() * 2), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
                                               w.rank_hi - w.rank_lo, w.stats.p);
     count_launch();
     const bool gs_like = algo != CHROMA_ALGO_JACOBI;
@@ -603,11 +610,13 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
       rt_mark("broadcast_losers");
     } else {
       run_detect(da, w.NL, w.det, w.stats.p, s);
+      rt_mark("detect");
     }
 #ifdef CHROMA_WITH_NCCL
     if (remote)
       NCCL_CHECK(ncclAllReduce(w.stats.p, w.stats.p, nstats, ncclUint64, ncclSum, w.comm, s));
 #endif
+    rt_mark("allreduce");
     CUDA_CHECK(cudaEventRecord(ev[3], s));
     CUDA_CHECK(cudaMemcpyAsync(hs.data(), w.stats.p, sizeof(unsigned long long) * (nstats + 1),
                                cudaMemcpyDeviceToHost, s));
