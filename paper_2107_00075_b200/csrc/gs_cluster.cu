@@ -126,7 +126,8 @@ __global__ void k_slot_count(const i64* rowptr, const i32* col, const i32* v, i6
     }
     m = max(m, d);
   }
-  atomicMax(maxd, m);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(maxd, m);
 }
 
 __global__ void k_mark(const i32* v, i64 n, uint8_t* member) {

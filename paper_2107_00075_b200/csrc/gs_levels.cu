@@ -182,16 +182,24 @@ __global__ void k_chain_cut(const i64* rowptr, const i32* col, const i32* wl, i6
 // indeg[head] = lower worklist neighbours of the run's members outside the run
 __global__ void k_run_indeg(const i64* rowptr, const i32* col, const i32* wl, i64 n, const uint8_t* member,
                             const i32* head, i32* indeg) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    const i32 x = wl[i];
-    const i32 h = head[x];
+  // warp-aligned: a run's members are consecutive in wl, so lanes mostly share h
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 b = (blockIdx.x * (i64)blockDim.x + threadIdx.x) & ~31ll; b < n; b += stride) {
+    const i64 i = b + (threadIdx.x & 31);
+    i32 h = -1;
     int d = 0;
-    for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) {
-      const i32 u = col[e];
-      if (u >= h) break;
-      d += member[u];
+    if (i < n) {
+      const i32 x = wl[i];
+      h = head[x];
+      for (i64 e = rowptr[x]; e < rowptr[x + 1]; e++) {
+        const i32 u = col[e];
+        if (u >= h) break;
+        d += member[u];
+      }
     }
-    if (d) atomicAdd(indeg + h, d);
+    const unsigned grp = __match_any_sync(FULL, h);
+    d = (int)__reduce_add_sync(grp, (unsigned)d);
+    if (h >= 0 && d && (threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1)) atomicAdd(indeg + h, d);
   }
 }
 
@@ -229,12 +237,28 @@ __global__ void k_run_step(const i64* rowptr, const i32* col, const uint8_t* mem
     const i32 v = frontier[i];
     const i32 hv = head[v];
     const i64 rs = rowptr[v], re = rowptr[v + 1];
-    for (i64 e = re - 1 - lane; e >= rs; e -= 32) {
-      const i32 x = col[e];
-      if (x <= v) break;
-      if (!member[x]) continue;
-      const i32 h = head[x];
-      if (h != hv && atomicSub(indeg + h, 1) == 1) expand_run(h, runlen[h], (i32)lvl + 1, level, next, nnext);
+    // successors from the top of the sorted row, 32 at a time; lanes releasing the
+    // same run combine their decrements (mesh rows hit a few runs many times)
+    for (i64 base = re - 1; base >= rs; base -= 32) {
+      const i64 e = base - lane;
+      i32 h = -1;
+      bool more = false;
+      if (e >= rs) {
+        const i32 x = col[e];
+        if (x > v) {
+          more = true;
+          if (member[x]) {
+            const i32 hx = head[x];
+            if (hx != hv) h = hx;
+          }
+        }
+      }
+      const unsigned grp = __match_any_sync(FULL, h);
+      if (h >= 0 && lane == __ffs(grp) - 1) {
+        const int c = __popc(grp);
+        if (atomicSub(indeg + h, c) == c) expand_run(h, runlen[h], (i32)lvl + 1, level, next, nnext);
+      }
+      if (!__all_sync(FULL, more)) break;
     }
   }
 }
@@ -297,7 +321,8 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   CUDA_CHECK(cudaMemsetAsync(cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
   i64 lvl = 0;
   bool done = false;
-  const int grid = num_sms() * 8;
+  static const int grid_mult = std::getenv("CHROMA_LEVEL_GRID") ? std::atoi(std::getenv("CHROMA_LEVEL_GRID")) : 8;
+  const int grid = num_sms() * grid_mult;
   while (!done) {
     for (int k = 0; k < BATCH; k++, lvl++) {
       const int p = (int)(lvl & 1);

@@ -531,15 +531,25 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         // the cluster kernel resolves runs of adjacent consecutive ids in one level
         const bool chains = try_cluster && !no_chains;
         std::vector<i64> lsizes;
+        static const bool ltrace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
+        const auto lt0 = std::chrono::steady_clock::now();
         w.level_mode = (sched == 0 || sched == 1) && w.delta_max <= level_max_deg &&
                        build_level_order(w.g.rowptr.p, w.g.col.p, w.NL, w.cs.wl.p, owned, w.level_wl, n, s,
                                          &lsizes, try_cluster ? 1 : -1, chains);
+        const auto lt1 = std::chrono::steady_clock::now();
         if (w.level_mode && try_cluster &&
             !build_cluster_plan(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, w.level_wl.p, n, lsizes, w.cplan, s,
                                 chains, !hubs_done)) {
           // no cluster: keep the schedule only if it is wide enough for the dataflow
           // kernel (and has no runs, which only the cluster kernel evaluates)
           if (chains || (i64)lsizes.size() * 2048 > owned) w.level_mode = false;
+        }
+        if (ltrace) {
+          CUDA_CHECK(cudaStreamSynchronize(s));
+          const auto lt2 = std::chrono::steady_clock::now();
+          std::fprintf(stderr, "[levels] build %.2f ms, cluster plan %.2f ms\n",
+                       std::chrono::duration<double, std::milli>(lt1 - lt0).count(),
+                       std::chrono::duration<double, std::milli>(lt2 - lt1).count());
         }
         w.level_n = w.level_mode ? n : 0;
         if (!w.level_mode && (sched == 0 || sched == 2) &&

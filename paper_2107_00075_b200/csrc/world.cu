@@ -44,17 +44,47 @@ __global__ void k_block_owner(i32* owner, i64 n, i32 P) {
 }
 
 // chk[0] += out-of-range owners, chk[1] = max degree, chk[2 + r] += |owned(r)|
+// owner range, per-rank counts and the maximum degree.  Counts go through a block
+// histogram (P <= 1024) or warp-aggregated atomics; the maximum is warp-reduced.
 __global__ void k_owner_check(const i32* owner, i64 n, i32 P, const i64* off, unsigned long long* chk) {
-  unsigned long long bad = 0, dmax = 0;
-  for (i64 v = blockIdx.x * (i64)blockDim.x + threadIdx.x; v < n; v += (i64)gridDim.x * blockDim.x) {
-    const i32 o = owner[v];
-    if (o < 0 || o >= P) bad++;
-    else if (P <= 4096) atomicAdd(&chk[2 + o], 1ull);
-    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
-    dmax = d > dmax ? d : dmax;
+  __shared__ unsigned h[1024];
+  const bool local = P <= 1024;
+  if (local)
+    for (int i = threadIdx.x; i < P; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  unsigned long long bad = 0;
+  unsigned dmax = 0;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 b = (blockIdx.x * (i64)blockDim.x + threadIdx.x) & ~31ll; b < n; b += stride) {
+    const i64 v = b + (threadIdx.x & 31);
+    i32 o = -1;
+    if (v < n) {
+      o = owner[v];
+      if (o < 0 || o >= P) {
+        bad++;
+        o = -1;
+      }
+      const i64 d = off[v + 1] - off[v];
+      dmax = max(dmax, d > 0xffffffffll ? 0xffffffffu : (unsigned)d);
+    }
+    if (P <= 4096) {
+      const unsigned grp = __match_any_sync(0xffffffffu, o);
+      if (o >= 0 && (threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1)) {
+        if (local) atomicAdd(&h[o], (unsigned)__popc(grp));
+        else atomicAdd(&chk[2 + o], (unsigned long long)__popc(grp));
+      }
+    }
   }
-  if (bad) atomicAdd(&chk[0], bad);
-  atomicMax(&chk[1], dmax);
+  dmax = __reduce_max_sync(0xffffffffu, dmax);
+  const unsigned nbad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (nbad) atomicAdd(&chk[0], (unsigned long long)nbad);
+    atomicMax(&chk[1], (unsigned long long)dmax);
+  }
+  __syncthreads();
+  if (local)
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+      if (h[i]) atomicAdd(&chk[2 + i], (unsigned long long)h[i]);
 }
 
 // owned_lid[list[i]] = i (position of each owned gid inside its owner)
@@ -178,8 +208,15 @@ __global__ void k_bound1(const i64* lrow, const i32* lcol, i64 nl, i64 oc, uint8
       eg += (unsigned long long)(re - rs);
     }
   }
-  atomicAdd(&ecount[0], el);
-  atomicAdd(&ecount[1], eg);
+  // one atomic pair per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    el += __shfl_down_sync(0xffffffffu, el, o);
+    eg += __shfl_down_sync(0xffffffffu, eg, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&ecount[0], el);
+    atomicAdd(&ecount[1], eg);
+  }
 }
 
 // boundary_d2 = boundary_d1 u owned vertices with an owned boundary_d1 neighbour
@@ -327,7 +364,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       DBuf<unsigned long long> chk;
       chk.alloc(P + 2, s);
       chk.zero(s);
-      k_owner_check<<<G(n), 256, 0, s>>>(owner.p, n, P, goff.p, chk.p);
+      k_owner_check<<<std::min(G(n), num_sms() * 4), 256, 0, s>>>(owner.p, n, P, goff.p, chk.p);
       count_launch();
       std::vector<unsigned long long> hc((size_t)P + 2);
       CUDA_CHECK(cudaMemcpyAsync(hc.data(), chk.p, sizeof(unsigned long long) * (P + 2), cudaMemcpyDeviceToHost, s));
