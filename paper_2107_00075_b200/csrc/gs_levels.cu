@@ -156,6 +156,8 @@ __global__ void __launch_bounds__(1024) k_run_heads(i64 nv, const uint8_t* membe
     head[x] = h;
     const bool last = x + 1 >= nv || (t == 1023) || !cont[x + 1];
     if (last) runlen[h] = (i32)(x - h + 1);
+  } else if (x < nv) {
+    head[x] = -1;  // non-members (ghosts): k_run_step tests membership through head alone
   }
 }
 
@@ -247,16 +249,29 @@ __global__ void k_run_step(const i64* rowptr, const i32* col, const uint8_t* mem
         const i32 x = col[e];
         if (x > v) {
           more = true;
-          if (member[x]) {
-            const i32 hx = head[x];
-            if (hx != hv) h = hx;
-          }
+          const i32 hx = head[x];  // -1 for non-members: one dependent load, not two
+          if (hx >= 0 && hx != hv) h = hx;
         }
       }
       const unsigned grp = __match_any_sync(FULL, h);
+      bool rel = false;
+      i32 len = 0;
+      unsigned long long b = 0;
       if (h >= 0 && lane == __ffs(grp) - 1) {
         const int c = __popc(grp);
-        if (atomicSub(indeg + h, c) == c) expand_run(h, runlen[h], (i32)lvl + 1, level, next, nnext);
+        len = runlen[h];  // issued alongside the atomic, not after it
+        rel = atomicSub(indeg + h, c) == c;
+        if (rel) b = atomicAdd(nnext, (unsigned long long)len);
+      }
+      // released runs are written out by the whole warp (runs are up to 1024 ids)
+      for (unsigned rm = __ballot_sync(FULL, rel); rm; rm &= rm - 1) {
+        const int src = __ffs(rm) - 1;
+        const i32 hh = __shfl_sync(FULL, h, src), ll = __shfl_sync(FULL, len, src);
+        const unsigned long long bb = __shfl_sync(FULL, b, src);
+        for (i32 k = lane; k < ll; k += 32) {
+          next[bb + k] = hh + k;
+          level[hh + k] = (i32)lvl + 1;
+        }
       }
       if (!__all_sync(FULL, more)) break;
     }
