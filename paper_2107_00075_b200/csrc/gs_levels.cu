@@ -15,6 +15,7 @@
 // evaluation order differs.  Deep, narrow DAGs (average level < 2048 vertices) keep
 // the id order, where the kernel resolves chains inside a warp (C2: 890 levels of
 // ~2,400 vertices -> levels; C1 and R-MAT -> id order).
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -331,7 +332,10 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   DBuf<unsigned long long> dsz;
   dsz.alloc(cap_levels + 1, s);
   dsz.zero(s);
-  std::vector<unsigned long long> hsz((size_t)cap_levels + 1, 0);
+  // host copy grows by BATCH per check (cap_levels is nwl when the caller allows any
+  // depth: zero-filling that up front cost ~2 ms of host time per build)
+  std::vector<unsigned long long> hsz;
+  const auto tl0 = std::chrono::steady_clock::now();
   i32* buf[2] = {fa.p, fb.p};
   CUDA_CHECK(cudaMemsetAsync(cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
   i64 lvl = 0;
@@ -349,8 +353,9 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
                                           buf[p ^ 1], dsz.p);
     }
     count_launch(BATCH);
-    CUDA_CHECK(cudaMemcpyAsync(hsz.data(), dsz.p, sizeof(unsigned long long) * (size_t)lvl, cudaMemcpyDeviceToHost,
-                               s));
+    hsz.resize((size_t)lvl);
+    CUDA_CHECK(cudaMemcpyAsync(hsz.data() + (lvl - BATCH), dsz.p + (lvl - BATCH), sizeof(unsigned long long) * BATCH,
+                               cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
     done = hsz[(size_t)lvl - 1] == 0;
     if (!done && lvl > max_levels) {  // deep and narrow: id order is better
@@ -369,9 +374,11 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   CHROMA_REQUIRE(seen == nwl, CHROMA_ERUNTIME, "level schedule did not cover the worklist");
   const i64 L = (i64)sizes.size();
   if (sizes_out) *sizes_out = sizes;
+  const auto tl1 = std::chrono::steady_clock::now();
   if (trace)
-    std::fprintf(stderr, "[levels] %lld levels for %lld vertices%s\n", (long long)L, (long long)nwl,
-                 chains ? " (runs)" : "");
+    std::fprintf(stderr, "[levels] %lld levels for %lld vertices%s, level loop %.2f ms\n", (long long)L,
+                 (long long)nwl, chains ? " (runs)" : "",
+                 std::chrono::duration<double, std::milli>(tl1 - tl0).count());
   std::vector<i64> start((size_t)L), pstart((size_t)L);
   i64 a = 0, b = 0;
   for (i64 l = 0; l < L; l++) {

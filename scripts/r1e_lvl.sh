@@ -1,5 +1,5 @@
 #!/bin/bash
-# 1 GPU: run level build with one dependent head load and warp-wide run expansion
+# 1 GPU: run level build (head membership, warp-wide expansion, lazily grown host size copy)
 O=gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q > $O/l_pytest.log 2>&1; echo "pytest rc=$?" >> $O/l_pytest.log
 CHROMA_LEVEL_TRACE=1 timeout 300 python scripts/probe_e2e.py 2>&1 | grep -E "levels|h2d|level" | tail -3 > $O/l_e2e.log 2>&1
