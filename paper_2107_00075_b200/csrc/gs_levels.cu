@@ -226,18 +226,22 @@ __global__ void k_run_sources(const i32* wl, i64 n, const uint8_t* cont, const i
 // as k_level_step over runs: a run is released when its last outside dependency is
 __global__ void k_run_step(const i64* rowptr, const i32* col, const uint8_t* member, const i32* head,
                            const i32* runlen, const i32* frontier, unsigned long long* cnt, i64 lvl, i32* indeg,
-                           i32* level, i32* next, unsigned long long* sizes) {
+                           i32* level, i32* next, unsigned long long* sizes, i64 cap) {
   const int lane = threadIdx.x & 31;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  // the warp's first frontier entry is loaded before the level size is known (the
+  // buffer holds cap entries; the value is used only if warp < n): one dependent
+  // load fewer per level
+  const i32 v0 = warp < cap ? frontier[warp] : 0;
   const i64 n = (i64)cnt[lvl % 3];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     sizes[lvl] = (unsigned long long)n;
     cnt[(lvl + 2) % 3] = 0;
   }
   unsigned long long* nnext = cnt + (lvl + 1) % 3;
-  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
   for (i64 i = warp; i < n; i += nwarps) {
-    const i32 v = frontier[i];
+    const i32 v = i == warp ? v0 : frontier[i];
     const i32 hv = head[v];
     const i64 rs = rowptr[v], re = rowptr[v + 1];
     // successors from the top of the sorted row, 32 at a time; lanes releasing the
@@ -347,7 +351,7 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
       const int p = (int)(lvl & 1);
       if (chains)
         k_run_step<<<grid, 256, 0, s>>>(rowptr, col, member.p, head.p, runlen.p, buf[p], cnt.p, lvl, indeg.p,
-                                        level.p, buf[p ^ 1], dsz.p);
+                                        level.p, buf[p ^ 1], dsz.p, nwl);
       else
         k_level_step<<<grid, 256, 0, s>>>(rowptr, col, member.p, buf[p], cnt.p, lvl, indeg.p, level.p,
                                           buf[p ^ 1], dsz.p);
