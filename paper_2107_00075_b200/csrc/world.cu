@@ -139,23 +139,34 @@ __device__ __forceinline__ bool keep_nbr(i64 lid, i64 oc, i64 l1, int gl, uint8_
 
 __global__ void k_rowlen(const i32* lgids, i64 nl, i64 oc, i64 l1, int gl, const i64* goff,
                          const i32* gcol, const uint8_t* cls, i64* len) {
+  // a warp takes 32 consecutive rows: complete rows (owned; layer 1 with two layers)
+  // are a lane's length lookup, the partial ones are counted by the whole warp
   const int lane = threadIdx.x & 31;
   const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  for (i64 lid = warp; lid < nl; lid += nwarps) {
-    const i32 g = lgids[lid];
-    const i64 rs = goff[g], re = goff[g + 1];
-    i64 c = 0;
-    if (lid < oc || (lid < oc + l1 && gl == 2)) {
-      c = re - rs;
-    } else {
-      for (i64 e0 = rs; e0 < re; e0 += 32) {
+  for (i64 b = warp * 32; b < nl; b += nwarps * 32) {
+    const i64 lid = b + lane;
+    i64 rs = 0, re = 0;
+    bool partial = false;
+    if (lid < nl) {
+      const i32 g = lgids[lid];
+      rs = goff[g];
+      re = goff[g + 1];
+      if (lid < oc || (lid < oc + l1 && gl == 2)) len[lid] = re - rs;
+      else partial = true;
+    }
+    for (unsigned pm = __ballot_sync(FULL, partial); pm; pm &= pm - 1) {
+      const int src = __ffs(pm) - 1;
+      const i64 plid = b + src;
+      const i64 prs = __shfl_sync(FULL, rs, src), pre = __shfl_sync(FULL, re, src);
+      i64 c = 0;
+      for (i64 e0 = prs; e0 < pre; e0 += 32) {
         const i64 e = e0 + lane;
-        const bool k = e < re && keep_nbr(lid, oc, l1, gl, cls[gcol[e]]);
+        const bool k = e < pre && keep_nbr(plid, oc, l1, gl, cls[gcol[e]]);
         c += __popc(__ballot_sync(FULL, k));
       }
+      if (lane == 0) len[plid] = c;
     }
-    if (lane == 0) len[lid] = c;
   }
 }
 
@@ -170,6 +181,26 @@ __global__ void k_fill(const i32* lgids, i64 nl, i64 oc, i64 l1, int gl, const i
     const i32 g = lgids[lid];
     const i64 rs = goff[g], re = goff[g + 1];
     i64 pos = lrow[lid];
+    if (re - rs <= 32) {  // one chunk: load once, place all three classes from three ballots
+      const i64 e = rs + lane;
+      i32 u = 0;
+      uint8_t cu = 0;
+      if (e < re) {
+        u = gcol[e];
+        cu = cls[u];
+      }
+      const bool k = cu >= 1 && cu <= 3 && keep_nbr(lid, oc, l1, gl, cu);
+      const unsigned b1 = __ballot_sync(FULL, k && cu == 1), b2 = __ballot_sync(FULL, k && cu == 2),
+                     b3 = __ballot_sync(FULL, k && cu == 3);
+      if (k) {
+        const unsigned lt = lanemask_lt();
+        const int off = cu == 1   ? __popc(b1 & lt)
+                        : cu == 2 ? __popc(b1) + __popc(b2 & lt)
+                                  : __popc(b1) + __popc(b2) + __popc(b3 & lt);
+        lcol[pos + off] = lid_of[u];
+      }
+      continue;
+    }
     for (uint8_t c = 1; c <= 3; c++) {
       for (i64 e0 = rs; e0 < re; e0 += 32) {
         const i64 e = e0 + lane;
