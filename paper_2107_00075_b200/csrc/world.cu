@@ -98,6 +98,43 @@ __global__ void k_i64_to_i32(const i64* in, i32* out, i64 n) {
     out[i] = (i32)in[i];
 }
 
+// out[0] = min, out[1] = max, out[2] = count of the gids owned by ranks [lo, hi)
+__global__ void k_owned_range(const i32* owner, i64 n, i32 lo, i32 hi, unsigned long long* out) {
+  unsigned long long mn = ~0ull, mx = 0, c = 0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    if (owner[i] >= lo && owner[i] < hi) {
+      mn = min(mn, (unsigned long long)i);
+      mx = max(mx, (unsigned long long)i);
+      c++;
+    }
+  mn = __reduce_min_sync(0xffffffffu, (unsigned)min(mn, 0xffffffffull));
+  mx = __reduce_max_sync(0xffffffffu, (unsigned)mx);
+  c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+  if ((threadIdx.x & 31) == 0) {
+    if (c) {
+      atomicMin(out, mn);
+      atomicMax(out + 1, mx);
+    }
+    atomicAdd(out + 2, c);
+  }
+}
+
+// out[0] = min, out[1] = max column over col[0, k)
+__global__ void k_col_range(const i32* col, i64 k, unsigned* out) {
+  unsigned mn = ~0u, mx = 0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < k; i += (i64)gridDim.x * blockDim.x) {
+    const unsigned u = (unsigned)col[i];
+    mn = min(mn, u);
+    mx = max(mx, u);
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, mn);
+    atomicMax(out + 1, mx);
+  }
+}
+
 __global__ void k_flag_eq_i32(const i32* a, i64 n, i32 v, uint8_t* flag) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
     flag[i] = a[i] == v ? 1 : 0;
@@ -413,12 +450,63 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       const i64 CH = (i64)1 << 26;
       DBuf<i64> tmp;
       tmp.alloc(std::min<i64>(std::max<i64>(nnz, 1), CH), s);
-      for (i64 b = 0; b < nnz; b += CH) {
-        const i64 k = std::min(CH, nnz - b);
-        CUDA_CHECK(cudaMemcpyAsync(tmp.p, h_col + b, sizeof(i64) * k, cudaMemcpyHostToDevice, s));
-        k_i64_to_i32<<<G(k), 256, 0, s>>>(tmp.p, gcol.p + b, k);
+      auto upload = [&](i64 e0, i64 e1) {  // columns [e0, e1), converted to int32 in place
+        for (i64 b = e0; b < e1; b += CH) {
+          const i64 k = std::min(CH, e1 - b);
+          CUDA_CHECK(cudaMemcpyAsync(tmp.p, h_col + b, sizeof(i64) * k, cudaMemcpyHostToDevice, s));
+          k_i64_to_i32<<<G(k), 256, 0, s>>>(tmp.p, gcol.p + b, k);
+          count_launch();
+        }
+      };
+      // The builder reads the rows of the owned, layer-1 and (two layers) layer-2
+      // vertices only.  When the owned gids of [lo, hi) are one contiguous range (block
+      // partitions, one rank per process), only a gid window covering those rows
+      // crosses PCIe: it starts at the owned range and grows, once per ghost layer, by
+      // the neighbour range of the rows it added last.  Columns outside it are never read.
+      bool windowed = false;
+      static const bool no_window = std::getenv("CHROMA_NO_WINDOW") != nullptr;
+      if (hi - lo < P && n > 0 && !no_window) {
+        DBuf<unsigned long long> rr;
+        rr.alloc(3, s);
+        const unsigned long long init[3] = {~0ull, 0ull, 0ull};
+        CUDA_CHECK(cudaMemcpyAsync(rr.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        k_owned_range<<<std::min(G(n), num_sms() * 4), 256, 0, s>>>(owner.p, n, lo, hi, rr.p);
         count_launch();
+        unsigned long long hr[3];
+        CUDA_CHECK(cudaMemcpyAsync(hr, rr.p, sizeof(hr), cudaMemcpyDeviceToHost, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        if (hr[2] > 0 && hr[1] - hr[0] + 1 == hr[2]) {
+          windowed = true;
+          i64 g0 = (i64)hr[0], g1 = (i64)hr[1] + 1;
+          upload(h_off[g0], h_off[g1]);
+          i64 p[2][2] = {{g0, g1}, {g1, g1}};  // rows added last (up to two pieces)
+          DBuf<unsigned> cr;
+          cr.alloc(2, s);
+          for (int layer = 0; layer < gl; layer++) {
+            const unsigned cinit[2] = {~0u, 0u};
+            CUDA_CHECK(cudaMemcpyAsync(cr.p, cinit, sizeof(cinit), cudaMemcpyHostToDevice, s));
+            for (auto& q : p) {
+              const i64 e0 = h_off[q[0]], e1 = h_off[q[1]];
+              if (e1 > e0) {
+                k_col_range<<<std::min(G(e1 - e0), num_sms() * 4), 256, 0, s>>>(gcol.p + e0, e1 - e0, cr.p);
+                count_launch();
+              }
+            }
+            unsigned hc2[2];
+            CUDA_CHECK(cudaMemcpyAsync(hc2, cr.p, sizeof(hc2), cudaMemcpyDeviceToHost, s));
+            CUDA_CHECK(cudaStreamSynchronize(s));
+            if (hc2[0] > hc2[1]) break;  // no neighbours: nothing further is read
+            const i64 ng0 = std::min<i64>(g0, (i64)hc2[0]), ng1 = std::max<i64>(g1, (i64)hc2[1] + 1);
+            upload(h_off[ng0], h_off[g0]);
+            upload(h_off[g1], h_off[ng1]);
+            p[0][0] = ng0; p[0][1] = g0;
+            p[1][0] = g1; p[1][1] = ng1;
+            g0 = ng0;
+            g1 = ng1;
+          }
+        }
       }
+      if (!windowed) upload(0, nnz);
     }
     ptm.mark("col h2d+convert");
     DBuf<i32> owned_lid, lid_of;
