@@ -174,6 +174,28 @@ int chroma_world_colors_device(chroma_world* w, int32_t rank, int32_t** dev_ptr,
  * rounds), out[2] colour phase, out[3] exchange phase, out[4] detect phase. */
 int chroma_world_last_timing(chroma_world* w, double* out5);
 
+/* ---------------------------------------------------------------- generators */
+/* Synthetic BASELINE inputs built on `device` straight into int64 CSR (device
+ * pointers): sorted, simple, symmetric rows as chroma/graph.py:166-179 preprocess
+ * leaves them.  Counter-based draws (mix64 = the gid_rand finaliser of
+ * chroma/protocol.py:79-88) so that graph.py's NumPy path and the C oracle build the
+ * identical graph; the exact recipe is in csrc/gen.cu and DESIGN.md.
+ *   chroma_gen_rmat: Graph500 R-MAT, 2^scale vertices, edge_factor * 2^scale draws,
+ *     level thresholds t_* = floor(p * 2^32) for a, a+b, a+b+c; labels permuted when
+ *     `permute`.  col must hold 2 * edge_factor * 2^scale entries.
+ *   chroma_gen_random_bipartite: rows x rows pattern with nnz_per_row uniform
+ *     columns per row -> preprocess_directed -> to_bipartite (chroma/graph.py:182-188,
+ *     388-399): 2*rows vertices.  col must hold 2 * rows * nnz_per_row entries.
+ *   chroma_gen_box: kind 0 = gen_hex_mesh(nx, ny, nz) (chroma/graph.py:320-341),
+ *     kind 1 = 27-point stencil; call with col NULL to learn *nnz_out first. */
+int chroma_gen_rmat(int32_t scale, int64_t edge_factor, uint64_t seed, uint32_t t_a, uint32_t t_ab,
+                    uint32_t t_abc, int permute, int device, int64_t* row_offsets, int64_t* col_indices,
+                    int64_t* nnz_out);
+int chroma_gen_random_bipartite(int64_t rows, int64_t nnz_per_row, uint64_t seed, int device,
+                                int64_t* row_offsets, int64_t* col_indices, int64_t* nnz_out);
+int chroma_gen_box(int32_t kind, int64_t nx, int64_t ny, int64_t nz, int device, int64_t* row_offsets,
+                   int64_t* col_indices, int64_t* nnz_out);
+
 /* Number of kernels this library launched on `w` (or globally if w is NULL). */
 int64_t chroma_launch_count(void);
 

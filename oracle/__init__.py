@@ -17,12 +17,14 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 SRC = os.path.join(HERE, "chroma_oracle.c")
+SRCS = (SRC, os.path.join(HERE, "chroma_gen.c"))
 
 MODES = {"d1": 0, "d1-2gl": 1, "d2": 2, "pd2": 3}
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(SRC):
+    if force or not os.path.exists(LIB_PATH) or any(os.path.getmtime(LIB_PATH) < os.path.getmtime(x)
+                                                     for x in SRCS):
         subprocess.check_call(["make", "-C", HERE, "-s"])
     return LIB_PATH
 
@@ -58,6 +60,10 @@ def lib():
         L.orc_reset_exchange.argtypes = [P]
         L.orc_exchange.argtypes = [P, P, C.c_int, P, P]
         L.orc_run_distributed.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P, i64, P]
+        L.orc_gen_rmat.restype = i64
+        L.orc_gen_rmat.argtypes = [C.c_int, i64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, P, P]
+        L.orc_gen_bipartite.restype = i64
+        L.orc_gen_bipartite.argtypes = [i64, i64, C.c_uint64, P, P]
         L.orc_verify.restype = i64
         L.orc_verify.argtypes = [i64, P, P, P, P, C.c_int, P, i64]
         _lib = L
@@ -219,3 +225,24 @@ class World:
         if st == 4:
             raise RuntimeError("internal sweep tripwire")
         return colors, reports
+
+
+def gen_rmat(scale: int, edge_factor: int = 16, seed: int = 1, thresholds=None, permute: bool = True):
+    """(row_offsets, col_indices) of the counter-based R-MAT (oracle/chroma_gen.c)."""
+    if thresholds is None:
+        a, b, c = 0.57, 0.19, 0.19
+        t = float(1 << 32)
+        thresholds = (int(a * t), int((a + b) * t), int((a + b + c) * t))
+    n = 1 << scale
+    off = np.zeros(n + 1, dtype=np.int64)
+    col = np.empty(2 * edge_factor * n, dtype=np.int64)
+    nnz = lib().orc_gen_rmat(scale, edge_factor, seed, *thresholds, int(permute), _p(off), _p(col))
+    return off, col[:nnz]
+
+
+def gen_bipartite(rows: int, nnz_per_row: int = 32, seed: int = 3):
+    """(row_offsets, col_indices) of the counter-based random bipartite PD2 input."""
+    off = np.zeros(2 * rows + 1, dtype=np.int64)
+    col = np.empty(max(2 * rows * nnz_per_row, 1), dtype=np.int64)
+    nnz = lib().orc_gen_bipartite(rows, nnz_per_row, seed, _p(off), _p(col))
+    return off, col[:nnz]

@@ -70,6 +70,9 @@ def lib():
         "chroma_world_colors_device": (I, [P, i32, C.POINTER(P), PI64]),
         "chroma_world_last_timing": (I, [P, P]),
         "chroma_launch_count": (i64, []),
+        "chroma_gen_rmat": (I, [i32, i64, C.c_uint64, u32, u32, u32, I, I, P, P, PI64]),
+        "chroma_gen_random_bipartite": (I, [i64, i64, C.c_uint64, I, P, P, PI64]),
+        "chroma_gen_box": (I, [i32, i64, i64, i64, I, P, P, PI64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -88,7 +91,7 @@ EXPORTS = ("chroma_last_error", "chroma_version", "chroma_device_count", "chroma
            "chroma_world_connect", "chroma_world_global_degrees", "chroma_world_reset_exchange",
            "chroma_world_exchange", "chroma_world_color", "chroma_world_detect",
            "chroma_run_distributed", "chroma_world_colors_device", "chroma_world_last_timing",
-           "chroma_launch_count")
+           "chroma_launch_count", "chroma_gen_rmat", "chroma_gen_random_bipartite", "chroma_gen_box")
 
 
 def check(status: int, what: str = "") -> None:

@@ -2,6 +2,7 @@
 // Every call catches C++ exceptions and maps them to the reference's exception
 // classes through status codes + a thread-local message.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "world.cuh"
@@ -114,30 +115,21 @@ int chroma_csr_create(int64_t n, const int64_t* off, const int64_t* col, int dev
       h->g.device = device;
       CUDA_CHECK(cudaStreamCreateWithFlags(&h->g.stream, cudaStreamNonBlocking));
       cudaStream_t s = h->g.stream;
-      std::vector<int64_t> ho;
-      const int64_t* offh = off;
       if (dev(flags)) {
-        ho.resize((size_t)n + 1);
-        CUDA_CHECK(cudaMemcpy(ho.data(), off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
-        offh = ho.data();
+        h->g.rowptr.alloc(n + 1, s);
+        CUDA_CHECK(cudaMemcpyAsync(h->g.rowptr.p, off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
+      } else {
+        h->g.rowptr.upload(off, n + 1, s);
       }
-      const i64 nnz = offh[n];
+      i64 nnz = 0;
+      CUDA_CHECK(cudaMemcpyAsync(&nnz, h->g.rowptr.p + n, sizeof(i64), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      CHROMA_REQUIRE(nnz >= 0, CHROMA_EVALUE, "row_offsets[n] must be >= 0");
       h->g.n = n;
       h->g.nnz = nnz;
-      h->g.rowptr.upload(offh, n + 1, s);
-      std::vector<i32> c((size_t)nnz);
-      std::vector<int64_t> hc;
-      const int64_t* colh = col;
-      if (dev(flags)) {
-        hc.resize((size_t)nnz);
-        if (nnz) CUDA_CHECK(cudaMemcpy(hc.data(), col, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
-        colh = hc.data();
-      }
-      for (i64 i = 0; i < nnz; i++) {
-        CHROMA_REQUIRE(colh[i] >= 0 && colh[i] < n, CHROMA_EVALUE, "col_indices out of range");
-        c[(size_t)i] = (i32)colh[i];
-      }
-      h->g.col.upload(c.data(), std::max<i64>(nnz, 1), s);
+      // narrowed and range-checked on the device (no host pass over the columns)
+      h->g.col.alloc(std::max<i64>(nnz, 1), s);
+      narrow_ids_checked(col, nnz, n, dev(flags), h->g.col.p, s, "col_indices out of range");
       CUDA_CHECK(cudaStreamSynchronize(s));
     } catch (...) {
       if (h->g.stream) cudaStreamDestroy(h->g.stream);
@@ -198,7 +190,10 @@ int chroma_serial_greedy(chroma_csr* h, const int64_t* order, int32_t* colors_ou
     L.ticket = S.ticket.p;
     L.dist = 1;
     L.nv = n;
-    if (n > 0) launch_gs(L, s);
+    static const bool no_chunked = std::getenv("CHROMA_NO_CHUNKED") != nullptr;
+    bool done = n == 0;
+    if (!done && !order && !no_chunked) done = launch_gs_chunked(L, n, true, S.chunked, s);
+    if (!done) launch_gs(L, s);
     CUDA_CHECK(cudaMemcpyAsync(colors_out, S.val.p, sizeof(i32) * n,
                                dev(flags) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));

@@ -26,6 +26,19 @@ struct GsLaunch {
   bool level_mode = false;     // wl is a padded level schedule (gs_levels.cu), D1 only
 };
 void launch_gs(const GsLaunch& L, cudaStream_t s);
+// Exact Gauss-Seidel (D1) by chunked fixed point (gs_chunked.cu); nwl = exact
+// worklist length.  false: a colour above 1024 appeared, the worklist is back at
+// PENDING and the caller takes launch_gs.
+struct ChunkedScratch {
+  DBuf<u32> pool;
+  DBuf<i32> heavy, iota, flag;
+  DBuf<unsigned> cnt;
+  DBuf<u32> desc;
+  DBuf<unsigned long long> pool_top;
+};
+// upper_zero: every neighbour above a worklist member contributes colour 0 (round 0:
+// nothing is coloured yet), so rows are read up to the vertex only.
+bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScratch& S, cudaStream_t s);
 bool launch_gs_d1(const GsLaunch& L, cudaStream_t s);  // false if not applicable
 
 // Jacobi sweep pieces (chroma/localcolor.py:214-227, 292-303)
@@ -87,6 +100,8 @@ void select_flagged_base(const uint8_t* flags, i64 n, i32 base, i32* out, i64* n
 void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* out, i64* n_out,
                            cudaStream_t s);
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s);
+void narrow_ids_checked(const i64* src, i64 k, i64 n, bool src_on_device, i32* out, cudaStream_t s,
+                        const char* what);
 void sort_i32(i32* keys, i64 n, cudaStream_t s);  // ascending, in place (non-negative keys)
 void sort_u64(u64* keys, i64 n, cudaStream_t s);  // ascending, in place
 

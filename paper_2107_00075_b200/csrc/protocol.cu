@@ -248,8 +248,25 @@ gauss_seidel:
       L.nwl_max = S.level_n;
       L.level_mode = S.level_mode;
     }
+    static const bool no_chunked = std::getenv("CHROMA_NO_CHUNKED") != nullptr;
+    const bool cluster = S.level_wl && S.level_mode && S.cplan && dist == 1 && !L.old;
+    if (dist == 1 && !cluster && !no_chunked) {
+      // chunked fixed point over the original worklist (gs_chunked.cu)
+      const i64 nexact = wl_sorted_unique && nwl != nullptr ? read_i64(nwl, s) : nwl_max;
+      GsLaunch C = L;
+      C.wl = wl;
+      C.nwl_dev = nwl;
+      C.nwl_max = nexact;
+      C.level_mode = false;
+      if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
+      if (launch_gs_chunked(C, nexact, S.upper_zero, S.chunked, s)) {
+        if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
+        if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
+        return;
+      }
+    }
     if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
-    if (S.level_wl && S.level_mode && S.cplan && dist == 1 && !L.old) {
+    if (cluster) {
       launch_gs_cluster(*S.cplan, L.val, L.old, s);
     } else {
       if (S.level_wl && S.level_mode && S.cplan && S.cplan->chains) {
@@ -515,7 +532,10 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     const bool gs_like = algo != CHROMA_ALGO_JACOBI;
     // round 0 colours every owned vertex: claim them by DAG level (cached per world)
     w.cs.level_wl = nullptr;
-    if (round == 0 && dist == 1 && gs_like && !no_levels) {
+    // The schedule is built from round 0's full owned worklist and cached per world:
+    // not when hubs were pre-coloured (the worklist then lacks them), and only for
+    // bounded degree (the cluster kernel); other graphs take gs_chunked.cu.
+    if (round == 0 && dist == 1 && gs_like && !no_levels && !hubs_done && w.delta_max <= 32) {
       if (w.level_n < 0) {
         i64 owned = 0;
         std::vector<i64> counts;
@@ -567,12 +587,14 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
       }
     }
     rt_mark("hubs+worklist");
+    w.cs.upper_zero = round == 0 && !hubs_done;  // nothing is coloured before round 0
     color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, nwl_host, true, dist, partial,
               algo, true, w.cs, s, gs_like ? ev[6] : nullptr, gs_like ? ev[7] : nullptr);
     rt_mark("color");
     w.cs.level_wl = nullptr;
     w.cs.cplan = nullptr;
     w.cs.keep_free = false;
+    w.cs.upper_zero = false;
     CUDA_CHECK(cudaEventRecord(ev[1], s));
     // exchange: every ghost takes its owner's colour; accounting is changed-only
     const bool listed = fast && round > 0;  // exchange and detection driven by lists

@@ -179,6 +179,46 @@ void sort_u64(u64* keys, i64 n, cudaStream_t s) {
     CUDA_CHECK(cudaMemcpyAsync(keys, db.Current(), sizeof(u64) * n, cudaMemcpyDeviceToDevice, s));
 }
 
+namespace {
+__global__ void k_narrow_checked(const i64* in, i32* out, i64 k, i64 n, unsigned* bad) {
+  unsigned b = 0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < k; i += (i64)gridDim.x * blockDim.x) {
+    const i64 x = in[i];
+    b |= (x < 0 || x >= n) ? 1u : 0u;
+    out[i] = (i32)x;
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+}  // namespace
+
+// int64 ids in [0, n) (host or device) -> int32 device array; ValueError (with
+// `what`) if any id is out of range.  Host sources cross PCIe in 512 MB chunks.
+void narrow_ids_checked(const i64* src, i64 k, i64 n, bool src_on_device, i32* out, cudaStream_t s,
+                        const char* what) {
+  if (k <= 0) return;
+  DBuf<unsigned> bad;
+  bad.alloc(1, s);
+  bad.zero(s);
+  if (src_on_device) {
+    k_narrow_checked<<<ew_grid(k), 256, 0, s>>>(src, out, k, n, bad.p);
+    count_launch();
+  } else {
+    const i64 CH = (i64)1 << 26;
+    DBuf<i64> tmp;
+    tmp.alloc(std::min(k, CH), s);
+    for (i64 b = 0; b < k; b += CH) {
+      const i64 c = std::min(CH, k - b);
+      CUDA_CHECK(cudaMemcpyAsync(tmp.p, src + b, sizeof(i64) * c, cudaMemcpyHostToDevice, s));
+      k_narrow_checked<<<ew_grid(c), 256, 0, s>>>(tmp.p, out + b, c, n, bad.p);
+      count_launch();
+    }
+  }
+  unsigned hb = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  CHROMA_REQUIRE(hb == 0, CHROMA_EVALUE, what);
+}
+
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s) {
   if (n <= 0) return;
   size_t bytes = 0;

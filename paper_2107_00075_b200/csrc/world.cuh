@@ -57,6 +57,8 @@ struct ColorScratch {
   DBuf<i64> level_n_dev;
   DBuf<i64> fcnt;
   FreeWaveScratch fw;
+  ChunkedScratch chunked;
+  bool upper_zero = false;  // gs_chunked: no neighbour above a member is coloured yet
 };
 
 // Global hub pre-colouring scratch (hubs.cu)
