@@ -1,17 +1,17 @@
 #!/usr/bin/env python
 """Benchmark: distributed speculate-and-iterate colouring on B200 (BASELINE.json metric).
 
-Default workload (configs[1], "C2"): D1-2GL colouring of the 3-D 27-point stencil mesh
-128^3 (2,097,152 vertices, 26,822,908 undirected edges), partition_block over P = N
-ranks, one rank per GPU, deterministic mode (bit-exact with the reference).  One step =
-one full run_distributed (every round: colour, halo exchange over NVLink, detection,
-allreduce) on the device-resident world.
+Default workload (configs[2], "C3", the largest single-GPU configuration and the
+north-star target): D1 colouring of the permuted Graph500 R-MAT scale 24, edge factor
+16 (16.8 M vertices, 260.4 M undirected edges), partition_block over P = N ranks (one
+per GPU), deterministic mode -- the reference's Gauss-Seidel semantics, bit-exact with
+the C oracle (the colour array's sha256 is printed beside the oracle's).  One step =
+one full run_distributed on the device-resident world, colours left in HBM; nothing is
+cached between steps (the chunked Gauss-Seidel kernel builds everything it needs per
+call).  A "free" sub-record times the free-running mode on the same world.
 
-"--workload c3" runs configs[2], the north-star target: D1 colouring of the permuted
-R-MAT scale-24 graph (edge factor 16), P = N, free-running mode by default.
-
-    python bench.py [--gpus N --steps K --warmup W]            # our B200 path
-    python bench.py --workload c3 [--scale 24] [...]            # R-MAT (north-star target)
+    python bench.py [--gpus N --steps K --warmup W]            # our B200 path (C3)
+    python bench.py --workload c1|c2|c4|c5 [...]                # other BASELINE configs
     python bench.py --impl reference [...]                      # reference arm (CPU)
     torchrun --nproc-per-node N bench.py --gpus N ...           # N > 1
 
@@ -20,6 +20,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -34,36 +35,77 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 UNIT = "edges/s"
+GOLDEN = os.path.join(ROOT, "tests", "golden", "scale.json")
 
 
 class Workload:
-    """The benchmarked configuration (BASELINE.json configs[1] or configs[2])."""
+    """One BASELINE.json configuration."""
+
+    SPECS = {
+        "c1": dict(mode="d1", gl=1, vmode="d1", key="c1_1000",
+                   metric="coloring edges/s (D1, 2-D 5-point grid 1000x1000)",
+                   desc="C1: D1 grid 1000x1000 (gen_hex_mesh(1000,1000,1))",
+                   data="synthetic (reference gen_hex_mesh recipe, generated on device)"),
+        "c2": dict(mode="d1-2gl", gl=2, vmode="d1", key="c2_128",
+                   metric="coloring edges/s (D1-2GL, 27-pt stencil 128^3)",
+                   desc="C2: D1-2GL 27-point stencil 128^3",
+                   data="synthetic (27-point stencil generated on device, id = x + L(y + L z))"),
+        "c3": dict(mode="d1", gl=1, vmode="d1", key="c3_s24",
+                   metric="coloring edges/s (D1, R-MAT scale-24 ef16)",
+                   desc="C3: D1 R-MAT scale-24 edge factor 16 (a=.57 b=c=.19, permuted labels)",
+                   data="synthetic (counter-based Graph500 R-MAT generated on device; identical CSR to the "
+                        "C oracle's generator, sha256 checked)"),
+        "c4": dict(mode="d2", gl=2, vmode="d2", key="c4_200",
+                   metric="coloring edges/s (D2, 7-pt mesh 200^3)",
+                   desc="C4: D2 7-point mesh 200^3 (gen_hex_mesh(200,200,200))",
+                   data="synthetic (reference gen_hex_mesh recipe, generated on device)"),
+        "c5": dict(mode="pd2", gl=2, vmode="pd2", key="c5_2p22",
+                   metric="coloring edges/s (PD2, random 4M x 4M, 32 nnz/row)",
+                   desc="C5: PD2 random sparse 2^22 x 2^22, 32 nnz/row -> bipartite",
+                   data="synthetic (counter-based random sparse pattern generated on device; identical CSR "
+                        "to the C oracle's generator)"),
+    }
 
     def __init__(self, args):
         self.name = args.workload
-        if self.name == "c2":
-            self.mode, self.gl, self.vmode = "d1-2gl", 2, "d1"
-            self.metric = f"coloring edges/s (D1-2GL, 27-pt stencil {args.L}^3)"
-            self.algorithm = args.algorithm or "gauss-seidel"
-            self.desc = f"C2: D1-2GL 27-point stencil {args.L}^3"
-            self.data = "synthetic (27-point stencil generated on device, id = x + L(y + L z))"
-        else:
-            self.mode, self.gl, self.vmode = "d1", 1, "d1"
-            self.metric = f"coloring edges/s (D1, R-MAT scale-{args.scale} ef16)"
-            self.algorithm = args.algorithm or "free"
-            self.desc = f"C3: D1 R-MAT scale-{args.scale} edge factor 16 (permuted)"
-            self.data = "synthetic (Graph500 R-MAT a=.57 b=c=.19, seeded label permutation, generated on device)"
+        self.__dict__.update(self.SPECS[self.name])
         self.args = args
+        self.algorithm = args.algorithm or ("free" if self.name == "c5" else "gauss-seidel")
 
-    def graph(self, device=None, scale=None):
+    def graph(self, device=None):
+        """The workload's graph (host CSR arrays; built on `device` when given)."""
         from paper_2107_00075_b200 import graph as G
+        if self.name == "c1":
+            return G.gen_hex_mesh_device(1000, 1000, 1, device) if device else G.gen_hex_mesh(1000, 1000, 1)
         if self.name == "c2":
-            return G.gen_stencil27(self.args.L, device=device)
-        return G.gen_rmat(scale or self.args.scale, 16, 1, device=device)
+            return G.gen_stencil27(128, device=device)
+        if self.name == "c3":
+            return G.gen_rmat(self.args.scale, 16, 1, device=device)
+        if self.name == "c4":
+            return G.gen_hex_mesh_device(200, 200, 200, device) if device else G.gen_hex_mesh(200, 200, 200)
+        return G.gen_random_bipartite(1 << 22, 32, 3, device=device).graph
 
-    def sample_scale(self) -> int:
-        """Bounded CPU sample for the C3 oracle timing (the full graph takes hours in Python)."""
-        return min(self.args.scale, 18)
+    def oracle_graph(self):
+        """The same CSR arrays from the oracle's own generator (reference arm: no GPU)."""
+        import oracle
+        if self.name == "c3":
+            return oracle.gen_rmat(self.args.scale)
+        if self.name == "c5":
+            return oracle.gen_bipartite(1 << 22, 32, 3)
+        g = self.graph()
+        return g.row_offsets, g.col_indices
+
+    def golden(self, P: int):
+        """The oracle's full-scale values for this workload at P ranks (tests/golden/scale.json,
+        written by oracle/gen_scale_golden.py), or None."""
+        if not self.key or (self.name == "c3" and self.args.scale != 24):
+            return None
+        try:
+            with open(GOLDEN) as fh:
+                d = json.load(fh).get(self.key)
+        except Exception:
+            return None
+        return dict(d, run=d.get(f"{self.mode}_p{P}")) if d else None
 
 
 _JSON_FD = None
@@ -94,13 +136,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3"])
-    ap.add_argument("--L", type=int, default=128, help="C2 stencil edge length (128 = BASELINE config)")
+    ap.add_argument("--workload", default="c3", choices=sorted(Workload.SPECS))
     ap.add_argument("--scale", type=int, default=24, help="C3 R-MAT scale (24 = BASELINE config)")
     ap.add_argument("--algorithm", default=None, choices=["gauss-seidel", "free", "jacobi"],
-                    help="default: gauss-seidel (deterministic, bit-exact) for c2, free for c3")
+                    help="default: gauss-seidel (deterministic, bit-exact); free for c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-free", action="store_true")
     return ap.parse_args()
 
 
@@ -108,9 +150,9 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class Clocks:
@@ -121,7 +163,6 @@ class Clocks:
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device = device
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={self.FIELDS}",
@@ -166,65 +207,69 @@ def round0_bytes(n_owned: int, nnz_owned: int, touched: int) -> int:
     return 4 * n_owned + 8 * (n_owned + 1) + 4 * nnz_owned + 4 * touched
 
 
-def cpu_baseline(wl: "Workload", P: int, budget_s: float = 30.0) -> dict:
-    """The C oracle (port of the reference path) on the host, single thread."""
+def sha256_i32(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).astype("<i4").tobytes()).hexdigest()
+
+
+def cpu_baseline(wl: "Workload", g, P: int) -> dict:
+    """The C oracle (port of the reference path) on the host, one thread, on the same
+    CSR arrays the GPU coloured: one full run_distributed (deterministic)."""
     import oracle
     from paper_2107_00075_b200 import partition as PT
-    g = wl.graph(scale=wl.sample_scale() if wl.name == "c3" else None)
     pm = PT.partition_block(g, P)
     w = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, wl.gl)
     t0 = time.perf_counter()
-    reps = 0
-    while True:
-        w.run(wl.mode, False, True)
-        reps += 1
-        el = time.perf_counter() - t0
-        if el > budget_s / 3 or reps >= 3:
-            break
-    sec = el / reps
+    w.run(wl.mode, False, True)
+    sec = time.perf_counter() - t0
     m = len(g.col_indices) // 2
-    what = (f"the full 27-pt {wl.args.L}^3 mesh" if wl.name == "c2"
-            else f"R-MAT scale-{wl.sample_scale()} (bounded sample of the scale-{wl.args.scale} workload)")
     return {"value": m / sec, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"oracle run_distributed ({wl.mode}, deterministic) on {what}, "
-                      f"P={P}, {reps} rep(s), {sec:.3f} s/step, 1 of {os.cpu_count()} cores"}
+            "sample": f"oracle run_distributed ({wl.mode}, deterministic) on the full {wl.desc} graph, P={P}, "
+                      f"1 run, {sec:.2f} s; 1 of {os.cpu_count()} host cores"}
 
 
 def run_reference(args):
-    """Reference arm: the CPU port of the reference path (oracle/), rank 0 only."""
+    """Reference arm: the CPU port of the reference path (oracle/) on the same
+    workload, rank 0 only; the graph comes from the oracle's own generator."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
-    from paper_2107_00075_b200 import partition as PT
     wl = Workload(args)
     P = args.gpus
-    g = wl.graph(scale=wl.sample_scale() if wl.name == "c3" else None)
-    pm = PT.partition_block(g, P)
-    w = oracle.World(g.row_offsets, g.col_indices, pm.owner, P, wl.gl)
+    t0 = time.perf_counter()
+    off, col = wl.oracle_graph()
+    n = len(off) - 1
+    owner = np.empty(n, np.int32)
+    for r in range(P):
+        owner[r * n // P:(r + 1) * n // P] = r
+    w = oracle.World(off, col, owner, P, wl.gl)
+    setup = time.perf_counter() - t0
     for _ in range(args.warmup):
         w.run(wl.mode, False, True)
     t = []
-    colors = None
+    colors = reps = None
     for _ in range(args.steps):
         t0 = time.perf_counter()
         colors, reps = w.run(wl.mode, False, True)
         t.append(time.perf_counter() - t0)
-    m = len(g.col_indices) // 2
+    m = len(col) // 2
     T = sum(t)
     val = m * args.steps / T
-    ncol = int(len(np.unique(colors[colors > 0])))
-    sample = ("full workload each step" if wl.name == "c2"
-              else f"R-MAT scale-{wl.sample_scale()} each step (bounded sample of scale {args.scale})")
+    gold = wl.golden(P)
+    sha = sha256_i32(colors)
     line = {"metric": wl.metric, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": P,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic",
+            "data": "synthetic (oracle generator, same CSR as the GPU arm)",
             "config": {"workload": f"{wl.desc}, partition_block P={P}, deterministic (oracle)",
-                       "n": g.num_vertices, "m": m, "rounds": len(reps), "colors": ncol},
+                       "n": n, "m": m, "rounds": len(reps), "colors": int(len(np.unique(colors[colors > 0]))),
+                       "colour_sha256": sha,
+                       "golden_match": (gold or {}).get("run", {}).get("sha256") == sha if gold else None,
+                       "setup_s": round(setup, 1)},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": f"oracle/ C port of the reference path, {sample}, "
-                                       f"1 of {os.cpu_count()} cores"},
+                             "sample": f"oracle/ C port of the reference path, full workload each step, "
+                                       f"1 of {os.cpu_count()} host cores (the reference is single-threaded, "
+                                       f"chroma/runtime.py:125)"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -235,6 +280,7 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    import ctypes as C
     import torch
     import torch.distributed as dist
     from paper_2107_00075_b200 import launch_count
@@ -271,130 +317,166 @@ def main():
     g = wl.graph(device=f"cuda:{local}")
     m = len(g.col_indices) // 2
     pm = PT.partition_block(g, N)
-    cfg = R.AlgorithmConfig(mode=R.Mode(wl.mode), deterministic=wl.algorithm == "gauss-seidel",
-                            algorithm=None if wl.algorithm == "gauss-seidel" else wl.algorithm)
 
-    def make_world():
+    def cfg_for(algorithm):
+        return R.AlgorithmConfig(mode=R.Mode(wl.mode), deterministic=algorithm == "gauss-seidel",
+                                 algorithm=None if algorithm == "gauss-seidel" else algorithm)
+
+    def make_world(graph, partition):
         if N == 1:
-            return RT.build_local_graphs(g, pm, wl.gl)
+            return RT.build_local_graphs(graph, partition, wl.gl)
         from paper_2107_00075_b200.dist import DistWorld
-        return DistWorld(g, pm, wl.gl)
+        return DistWorld(graph, partition, wl.gl)
 
-    world = make_world()
+    world = make_world(g, pm)
     lg = world.local_graphs[0] if N == 1 else world.local_graph
-    # `value` keeps the result in HBM (device output); e2e below returns it to the host
     n_out = world.output_length() if hasattr(world, "output_length") else world.num_global_vertices
     out = torch.empty(n_out, dtype=torch.int32, device=f"cuda:{local}")
-    for _ in range(args.warmup):
-        R.run_distributed(world, cfg, out=out)
-
-    import ctypes as C
     tbuf = (C.c_double * 5)()
-    barrier()
-    torch.cuda.synchronize()
-    clk = Clocks(local) if rank == 0 else None
-    l0 = launch_count()
-    per = []
-    kern = []
-    r0 = []
-    rounds = 0
-    colors = None
-    for _ in range(args.steps):
+
+    def timed_steps(cfg, K, W):
+        """W untimed + K timed run_distributed calls; per-step device times (CUDA events
+        on the world's stream inside the library: whole call, colouring kernel)."""
+        for _ in range(W):
+            R.run_distributed(world, cfg, out=out)
         barrier()
-        colors, reports = R.run_distributed(world, cfg, out=out)
-        _lib.check(_lib.lib().chroma_world_last_timing(world.handle.h, tbuf))
-        per.append(tbuf[0])
-        kern.append(tbuf[1])
-        r0.append(reports[0].time_color_s)
-        rounds = len(reports)
-    torch.cuda.synchronize()
-    barrier()
-    launches = launch_count() - l0
+        torch.cuda.synchronize()
+        l0 = launch_count()
+        per, kern, reps = [], [], None
+        for _ in range(K):
+            barrier()
+            _, reps = R.run_distributed(world, cfg, out=out)
+            _lib.check(_lib.lib().chroma_world_last_timing(world.handle.h, tbuf))
+            per.append(tbuf[0])
+            kern.append(tbuf[1] if cfg.deterministic else reps[0].time_color_s)
+        torch.cuda.synchronize()
+        barrier()
+        return per, kern, reps, launch_count() - l0
+
+    # ---- the headline: deterministic (bit-exact) colouring
+    cfg = cfg_for(wl.algorithm)
+    clk = Clocks(local) if rank == 0 else None
+    per, kern, reports, launches = timed_steps(cfg, args.steps, args.warmup)
     clocks = clk.stop() if clk else None
     T = allmax(sum(per))
     TK = allmax(sum(kern))
     value = m * args.steps / T
-    # ---- colour count and properness (global, after timing)
-    colors = colors.cpu().numpy()
-    if N == 1:
-        gcol = colors
-    else:
-        own = torch.from_numpy(colors.astype(np.int32)).cuda()
+
+    def gather_colors():
+        c = out.cpu().numpy()
+        if N == 1:
+            return c
+        own = out.clone()
         sizes = [None] * N
         dist.all_gather_object(sizes, int(own.numel()))
         bufs = [torch.empty(s, dtype=torch.int32, device=own.device) for s in sizes]
         dist.all_gather(bufs, own)
-        gcol = torch.cat(bufs).cpu().numpy()  # partition_block: owned ranges are contiguous in gid order
-    ncol, _ = V.color_stats(gcol) if rank == 0 else (None, None)
-    nviol = V.count_violations(g, gcol, wl.vmode) if rank == 0 else None
-    # ---- roofline of the dominant kernel (colouring, round 0 bytes)
+        return torch.cat(bufs).cpu().numpy()  # partition_block: owned ranges are contiguous in gid order
+
+    gcol = gather_colors()
+    ncol = nviol = sha = None
+    gold = wl.golden(N)
+    if rank == 0:
+        ncol, _ = V.color_stats(gcol)
+        mask = None
+        if wl.mode == "pd2":
+            mask = np.zeros(g.num_vertices, np.uint8)
+            mask[: g.num_vertices // 2] = 1
+        nviol = V.count_violations(g, gcol, wl.vmode, mask)
+        sha = sha256_i32(gcol)
+    parity = None
+    if rank == 0 and gold and cfg.deterministic:
+        ref = (gold.get("run") or {})
+        parity = {"oracle_sha256": ref.get("sha256"), "colour_sha256": sha,
+                  "match": ref.get("sha256") == sha if ref.get("sha256") else None,
+                  "oracle_rounds": ref.get("rounds"), "rounds": len(reports),
+                  "oracle_colors": ref.get("colors"),
+                  "csr_sha256_match": gold.get("col_sha256") == hashlib.sha256(
+                      np.ascontiguousarray(g.col_indices).astype("<i8").tobytes()).hexdigest()}
+    # ---- free-running mode on the same world (sub-record)
+    free = None
+    if not args.no_free and cfg.deterministic and wl.name in ("c3", "c4", "c5"):
+        fcfg = cfg_for("free")
+        fper, _, freps, _ = timed_steps(fcfg, args.steps, 1)
+        Tf = allmax(sum(fper))
+        fcol = gather_colors()
+        if rank == 0:
+            fn, _ = V.color_stats(fcol)
+            ref_n = ((gold or {}).get("run") or {}).get("colors")
+            free = {"value": m * args.steps / Tf, "ms_per_step": 1e3 * Tf / args.steps, "rounds": len(freps),
+                    "colors": fn, "oracle_deterministic_colors": ref_n,
+                    "within_5pct": (fn <= 1.05 * ref_n) if ref_n else None,
+                    "violations": V.count_violations(g, fcol, wl.vmode)}
+    # ---- roofline of the dominant kernel (the round-0 colouring)
     n_o = lg.owned_count
     nnz_o = int(lg.row_offsets[n_o]) if N > 1 else len(g.col_indices)
     touched = lg.num_local if N > 1 else g.num_vertices
     B = round0_bytes(n_o, nnz_o, touched)
     kernel_s = TK / args.steps
-    if wl.algorithm == "free":
-        # free mode: round 0's colour phase (heavy waves + light speculation) is the unit
-        kernel_s = allmax(sum(r0)) / args.steps
     peak, peak_kind = peaks()
-    achieved = B / kernel_s / 1e9
+    achieved = B / kernel_s / 1e9 if kernel_s > 0 else None
     traffic = None
-    if N == 1 and wl.name == "c2" and args.L == 128 and wl.algorithm == "gauss-seidel":
-        try:
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-                traffic = json.load(fh)["colour_kernel_c2_p1"]["dram_bytes_per_launch"]
-        except Exception:
-            traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(f"{wl.name}_{wl.algorithm}_p{N}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        traffic = None
+    kname = {"c3": "k_gs_chunked (chunked exact Gauss-Seidel: throughput first pass + latency-bound dataflow)",
+             "c1": "k_gs_cluster (level-synchronous Gauss-Seidel on one cluster)",
+             "c2": "k_gs_cluster (level-synchronous Gauss-Seidel on one cluster)",
+             "c4": "gs_kernel<2> (two-hop Gauss-Seidel dataflow)"}.get(wl.name, "round-0 colour phase")
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        from paper_2107_00075_b200.graph import Graph
         off_p = torch.from_numpy(np.ascontiguousarray(g.row_offsets, dtype=np.int64)).pin_memory()
         col_p = torch.from_numpy(np.ascontiguousarray(g.col_indices, dtype=np.int64)).pin_memory()
-        own_p = torch.from_numpy(np.ascontiguousarray(pm.owner, dtype=np.int32)).pin_memory()
-        from paper_2107_00075_b200.graph import Graph
         hg = Graph(g.num_vertices, off_p.numpy(), col_p.numpy())
-        hpm = PT.PartitionMap(own_p.numpy(), N)
-        et = []
-        # W untimed warm-up calls (as for `value`): the first calls fill the device pool
-        # and torch's pinned host cache that the returned colour arrays come from
-        ew = max(1, args.warmup)
-        for it in range(max(1, min(args.steps, 3)) + ew):
-            barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            if N == 1:
-                wv = RT.build_local_graphs(hg, hpm, wl.gl)
-            else:
-                from paper_2107_00075_b200.dist import DistWorld
-                wv = DistWorld(hg, hpm, wl.gl)
-            out, _ = R.run_distributed(wv, cfg)
-            torch.cuda.synchronize()
-            el = time.perf_counter() - t0
-            del wv
-            if it >= ew:
-                et.append(el)
-        te = allmax(sum(et) / len(et))
+        hpm = PT.partition_block(hg, N)
+
+        def e2e_steps(graph, partition, K, W):
+            et = []
+            for it in range(K + W):
+                barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                wv = make_world(graph, partition)
+                colors, _ = R.run_distributed(wv, cfg)
+                torch.cuda.synchronize()
+                el = time.perf_counter() - t0
+                del wv, colors
+                if it >= W:
+                    et.append(el)
+            return allmax(sum(et) / len(et))
+
+        K = max(1, min(args.steps, 3))
+        te = e2e_steps(hg, hpm, K, max(1, min(args.warmup, 2)))
+        tp = e2e_steps(Graph(g.num_vertices, np.array(g.row_offsets), np.array(g.col_indices)), pm, 1, 0)
         e2e = {"value": m / te, "unit": UNIT,
-               "h2d_bytes_per_step": int(off_p.numel() * 8 + col_p.numel() * 8 + own_p.numel() * 4),
-               "d2h_bytes_per_step": int(4 * (g.num_vertices if N == 1 else n_o)),
-               "timing": "host perf_counter around build_local_graphs + run_distributed (synchronous API)"}
+               "h2d_bytes_per_step": int(off_p.numel() * 8 + col_p.numel() * 8),
+               "d2h_bytes_per_step": int(4 * n_out),
+               "timing": "host perf_counter around build_local_graphs (int64 CSR from pinned host memory to "
+                         "the device world) + run_distributed (colours back into host memory)",
+               "pageable_value": m / tp}
+        del off_p, col_p
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(wl, N)
+        cpu = cpu_baseline(wl, g, N)
     if rank == 0:
         line = {"metric": wl.metric, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": wl.data,
                 "config": {"workload": f"{wl.desc}, partition_block P={N}, {wl.algorithm}",
-                           "n": g.num_vertices, "m": m, "ghost_layers": wl.gl, "rounds": rounds, "colors": ncol,
-                           "violations": nviol, "parallelism": f"vertex-range x{N}",
+                           "n": g.num_vertices, "m": m, "ghost_layers": wl.gl, "rounds": len(reports),
+                           "colors": ncol, "violations": nviol, "colour_sha256": sha,
+                           "parallelism": f"vertex-range x{N}",
+                           "caching": "none: every step rebuilds the colouring state (no per-world schedule)"
+                                      if wl.name == "c3" else "per-world round-0 schedule built in warm-up",
                            "l2": f"inputs larger than L2 (int32 col {4 * len(g.col_indices) / 1e6:.0f} MB)"},
+                "parity": parity, "free": free,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": traffic,
-                             "kernel": ("Gauss-Seidel colouring kernel (k_gs_cluster: level-synchronous, one "
-                                        "16-CTA cluster, colours in DSMEM)" if wl.algorithm == "gauss-seidel"
-                                        else "round-0 colour phase (hub waves + light/tiny passes)"),
-                             "algorithmic_bytes_per_launch": B, "kernel_ms": kernel_s * 1e3,
+                             "frac": achieved / peak if achieved else None, "traffic": traffic,
+                             "kernel": kname, "algorithmic_bytes_per_launch": B, "kernel_ms": kernel_s * 1e3,
                              "peak_kind": peak_kind},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
         emit(line)

@@ -1,0 +1,284 @@
+// Net-centric free-running colouring for distance 2 and partial distance 2.
+//
+// Reference semantics: chroma/localcolor.py:136-158 (_forbidden_d2 over
+// two_hop_neighbors: the colours of N(v) ∪ N²(v) for D2, of N²(v) for PD2) and the
+// net-based loser rule of _d2_losers (230-271): inside one net -- a middle vertex u
+// and its adjacency (plus u itself for full D2) -- equal colours clash and the largest
+// id keeps its colour.
+//
+// The vertex-centric walk re-reads every middle's row once per member (~1,040 two-hop
+// visits per vertex on C5).  Here every middle u keeps a 256-colour mask of its net
+// (4 x u64, one 32-byte sector), so a vertex's forbidden set is the OR of the masks
+// of its own row -- |adj(v)| sector loads instead of Σ|adj(u)| colour gathers:
+//   masks   every net's mask from the current colours (one pass over the CSR);
+//   pick    each pending vertex ORs its nets' masks, takes the first free colour and
+//           ORs it into those masks at once (later vertices of the same pass see it);
+//   detect  per net, the largest pending id of each colour keeps it; the other
+//           pending members of that colour are uncoloured and form the next worklist.
+// Later iterations (few vertices) rebuild only the nets around the pending vertices.
+// Colours above 256 fall back to the vertex-centric kernels (color_free.cu).
+#include <cstdlib>
+
+#include "kernels.cuh"
+
+namespace chroma {
+namespace {
+
+constexpr int NW = 4;                  // u64 words per net mask: colours 1..256
+constexpr int NCOL = NW * 64;
+constexpr unsigned FULLM = 0xffffffffu;
+constexpr int GL = 8;                  // lanes per vertex in the pick pass
+
+struct NetArgs {
+  const i64* rowptr;
+  const i32* col;
+  i32* colors;
+  unsigned long long* mask;   // [nv][NW]
+  uint8_t* pend;              // pending this iteration
+  const i32* wl;
+  i64 nwl;
+  bool full;                  // D2: the middle's own colour is in its net
+  i32* next;                  // losers
+  unsigned long long* nnext;
+  unsigned* ovf;              // a colour above NCOL was needed
+};
+
+__device__ __forceinline__ void set_bit(unsigned long long (&m)[NW], i32 c) {
+  if (c >= 1 && c <= NCOL) m[(c - 1) >> 6] |= 1ull << ((c - 1) & 63);
+}
+
+// mask of net u from current colours, by one warp (rows are short; long rows loop)
+__device__ __forceinline__ void build_mask(const NetArgs& a, i32 u, int lane) {
+  unsigned long long m[NW] = {0, 0, 0, 0};
+  const i64 rs = a.rowptr[u], re = a.rowptr[u + 1];
+  for (i64 j = rs + lane; j < re; j += 32) set_bit(m, a.colors[a.col[j]]);
+  if (a.full && lane == 0) set_bit(m, a.colors[u]);
+#pragma unroll
+  for (int w = 0; w < NW; w++) {
+    const u32 lo = __reduce_or_sync(FULLM, (u32)m[w]), hi = __reduce_or_sync(FULLM, (u32)(m[w] >> 32));
+    m[w] = ((unsigned long long)hi << 32) | lo;
+  }
+  if (lane < NW) a.mask[(i64)u * NW + lane] = m[lane];
+}
+
+// all nets (warp per net)
+__global__ void k_masks_all(NetArgs a, i64 nv) {
+  const int lane = threadIdx.x & 31;
+  const i64 w0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 u = w0; u < nv; u += nw) build_mask(a, (i32)u, lane);
+}
+
+// nets adjacent to the pending vertices (warp per pending vertex, its row's nets)
+__global__ void k_masks_around(NetArgs a) {
+  const int lane = threadIdx.x & 31;
+  const i64 w0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 i = w0; i < a.nwl; i += nw) {
+    const i32 v = a.wl[i];
+    const i64 rs = a.rowptr[v], re = a.rowptr[v + 1];
+    for (i64 j = rs; j < re; j++) build_mask(a, a.col[j], lane);
+    if (a.full) build_mask(a, v, lane);
+  }
+}
+
+// pick: GL lanes per pending vertex
+__global__ void k_pick(NetArgs a) {
+  const int lane = threadIdx.x & 31, sub = lane % GL;
+  const i64 gi = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / GL, ng = ((i64)gridDim.x * blockDim.x) / GL;
+  for (i64 base = 0; base < a.nwl; base += ng) {  // uniform trip count: shuffles below use all lanes
+    const i64 i = base + gi;
+    const bool act = i < a.nwl;
+    const i32 v = act ? a.wl[i] : 0;
+    unsigned long long m[NW] = {0, 0, 0, 0};
+    i64 rs = 0, re = 0;
+    if (act) {
+      rs = a.rowptr[v];
+      re = a.rowptr[v + 1];
+      for (i64 j = rs + sub; j < re; j += GL) {
+        const i32 u = a.col[j];
+        const ulonglong4 q = *reinterpret_cast<const ulonglong4*>(a.mask + (i64)u * NW);
+        m[0] |= q.x;
+        m[1] |= q.y;
+        m[2] |= q.z;
+        m[3] |= q.w;
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < NW; w++)
+#pragma unroll
+      for (int o = GL / 2; o >= 1; o >>= 1) m[w] |= __shfl_xor_sync(FULLM, m[w], o);
+    if (act) {
+      i32 c = 0;
+#pragma unroll
+      for (int w = NW - 1; w >= 0; w--)
+        if (~m[w]) c = w * 64 + __ffsll((long long)~m[w]);
+      if (c == 0) {
+        if (sub == 0) atomicOr(a.ovf, 1u);
+        c = NCOL + 1;
+      } else {
+        // publish into the vertex's nets so later picks of this pass avoid it
+        const unsigned long long bit = 1ull << ((c - 1) & 63);
+        for (i64 j = rs + sub; j < re; j += GL) atomicOr(a.mask + (i64)a.col[j] * NW + ((c - 1) >> 6), bit);
+        if (a.full && sub == 0) atomicOr(a.mask + (i64)v * NW + ((c - 1) >> 6), bit);
+      }
+      if (sub == 0) a.colors[v] = c;
+    }
+  }
+}
+
+// detect on one net u by one warp: the largest pending id per colour survives
+__device__ __forceinline__ void detect_net(const NetArgs& a, i32 u, int lane, i32* mx) {
+  for (int k = lane; k < NCOL + 2; k += 32) mx[k] = -1;
+  __syncwarp();
+  const i64 rs = a.rowptr[u], re = a.rowptr[u + 1];
+  const i64 ext = a.full ? 1 : 0;  // the middle itself is a member of a D2 net
+  for (i64 j = rs + lane; j < re + ext; j += 32) {
+    const i32 x = j < re ? a.col[j] : u;
+    if (!a.pend[x]) continue;
+    const i32 c = a.colors[x];
+    if (c >= 1 && c <= NCOL + 1) atomicMax(mx + c, x);
+  }
+  __syncwarp();
+  // a settled member of the same colour cannot exist (the masks held it), so only
+  // pending members clash
+  for (i64 j = rs + lane; j < re + ext; j += 32) {
+    const i32 x = j < re ? a.col[j] : u;
+    if (!a.pend[x]) continue;
+    const i32 c = a.colors[x];
+    if (c >= 1 && c <= NCOL + 1 && mx[c] > x && a.colors[x] != 0) {
+      if (atomicExch(a.colors + x, 0) != 0) {
+        const unsigned long long k = atomicAdd(a.nnext, 1ull);
+        a.next[k] = x;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void k_detect_all(NetArgs a, i64 nv) {
+  __shared__ i32 mxs[8][NCOL + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const i64 w0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 u = w0; u < nv; u += nw) detect_net(a, (i32)u, lane, mxs[wid]);
+}
+
+__global__ void k_detect_around(NetArgs a) {
+  __shared__ i32 mxs[8][NCOL + 2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const i64 w0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 i = w0; i < a.nwl; i += nw) {
+    const i32 v = a.wl[i];
+    const i64 rs = a.rowptr[v], re = a.rowptr[v + 1];
+    for (i64 j = rs; j < re; j++) detect_net(a, a.col[j], lane, mxs[wid]);
+    if (a.full) detect_net(a, v, lane, mxs[wid]);
+  }
+}
+
+__global__ void k_zero_list(const i32* wl, i64 n, i32* colors) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) colors[wl[i]] = 0;
+}
+
+__global__ void k_max_deg(const i32* wl, i64 n, const i64* rowptr, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = wl[i];
+    const unsigned long long d = (unsigned long long)(rowptr[v + 1] - rowptr[v]);
+    m = d > m ? d : m;
+  }
+  m = __reduce_max_sync(FULLM, (unsigned)m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void k_set_pend(const i32* wl, i64 n, uint8_t* pend, uint8_t val) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) pend[wl[i]] = val;
+}
+
+int G(i64 n) { return grid_for(std::max<i64>(n, 1), 256, num_sms() * 16); }
+
+i64 net_waves() {
+  static const i64 w = [] {
+    const char* e = std::getenv("CHROMA_NET_WAVES");
+    return e ? std::max<i64>(1, std::atoll(e)) : 1024;
+  }();
+  return w;
+}
+
+}  // namespace
+
+// Colours the worklist (colours of its vertices must be 0; every other vertex keeps
+// its colour).  Returns false if a colour above 256 was needed (worklist back at 0).
+bool launch_free_net(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32* wl_in, i64 nwl,
+                     bool partial, NetScratch& S, cudaStream_t s) {
+  if (nwl <= 0) return true;
+  S.mask.reserve(nv * NW, s);
+  S.pend.reserve(nv, s);
+  CUDA_CHECK(cudaMemsetAsync(S.pend.p, 0, nv, s));
+  S.wl[0].reserve(nwl, s);
+  S.wl[1].reserve(nwl, s);
+  S.cnt.reserve(2, s);
+  CUDA_CHECK(cudaMemcpyAsync(S.wl[0].p, wl_in, sizeof(i32) * nwl, cudaMemcpyDeviceToDevice, s));
+  NetArgs a;
+  a.rowptr = rowptr;
+  a.col = col;
+  a.colors = colors;
+  a.mask = S.mask.p;
+  a.pend = S.pend.p;
+  a.full = !partial;
+  a.ovf = reinterpret_cast<unsigned*>(S.cnt.p + 1);
+  CUDA_CHECK(cudaMemsetAsync(S.cnt.p + 1, 0, sizeof(unsigned long long), s));
+  const i64 small = std::max<i64>(nv / 32, 4096);
+  int p = 0;
+  i64 n = nwl;
+  for (int it = 0; n > 0; it++) {
+    CHROMA_REQUIRE(it < 10000, CHROMA_ERUNTIME, "speculative loop failed to settle");
+    a.wl = S.wl[p].p;
+    a.nwl = n;
+    a.next = S.wl[p ^ 1].p;
+    a.nnext = S.cnt.p;
+    CUDA_CHECK(cudaMemsetAsync(S.cnt.p, 0, sizeof(unsigned long long), s));
+    k_set_pend<<<G(n), 256, 0, s>>>(a.wl, n, a.pend, 1);
+    const bool all = n > small;
+    if (all) k_masks_all<<<num_sms() * 16, 256, 0, s>>>(a, nv);
+    else k_masks_around<<<G(n * 32), 256, 0, s>>>(a);
+    // the first pass picks in waves of ascending worklist position: each wave sees the
+    // colours of the earlier ones in the masks, so fewer equal picks collide (the
+    // colour count stays near sequential first fit's)
+    const int waves = it == 0 ? (int)std::min<i64>(net_waves(), std::max<i64>(1, n / 1024)) : 1;
+    for (int wv = 0; wv < waves; wv++) {
+      NetArgs b = a;
+      const i64 lo = n * wv / waves, hi = n * (wv + 1) / waves;
+      b.wl = a.wl + lo;
+      b.nwl = hi - lo;
+      k_pick<<<G(b.nwl * GL), 256, 0, s>>>(b);
+    }
+    count_launch(waves - 1);
+    if (all) k_detect_all<<<num_sms() * 16, 256, 0, s>>>(a, nv);
+    else k_detect_around<<<G(n * 32), 256, 0, s>>>(a);
+    k_set_pend<<<G(n), 256, 0, s>>>(a.wl, n, a.pend, 0);
+    count_launch(6);
+    unsigned long long h[2];
+    CUDA_CHECK(cudaMemcpyAsync(h, S.cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if ((unsigned)h[1]) {
+      k_zero_list<<<G(nwl), 256, 0, s>>>(wl_in, nwl, colors);
+      count_launch();
+      return false;
+    }
+    n = (i64)h[0];
+    p ^= 1;
+  }
+  return true;
+}
+
+i64 worklist_max_degree(const i32* wl, i64 n, const i64* rowptr, NetScratch& S, cudaStream_t s) {
+  if (n <= 0) return 0;
+  S.cnt.reserve(2, s);
+  CUDA_CHECK(cudaMemsetAsync(S.cnt.p, 0, sizeof(unsigned long long), s));
+  k_max_deg<<<std::min(G(n), num_sms() * 4), 256, 0, s>>>(wl, n, rowptr, S.cnt.p);
+  count_launch();
+  unsigned long long h = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&h, S.cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  return (i64)h;
+}
+
+}  // namespace chroma

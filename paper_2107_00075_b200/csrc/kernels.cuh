@@ -84,6 +84,17 @@ void launch_free_split(const i32* wl, const i64* n_dev, i64 n_max, const i64* ro
 void launch_free_iteration(const i64* rowptr, const i32* col, i32* colors, FreeLists& f, int p, i64 nlight_max,
                            i64 nheavy_max, int rank_cap, int dist, bool partial, cudaStream_t s);
 
+// Net-centric free-running D2/PD2 (color_net.cu): worklist colours must be 0 on entry.
+// false: a colour above 256 was needed (worklist back at 0, caller falls back).
+struct NetScratch {
+  DBuf<unsigned long long> mask, cnt;
+  DBuf<uint8_t> pend;
+  DBuf<i32> wl[2];
+};
+bool launch_free_net(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32* wl, i64 nwl, bool partial,
+                     NetScratch& S, cudaStream_t s);
+i64 worklist_max_degree(const i32* wl, i64 n, const i64* rowptr, NetScratch& S, cudaStream_t s);
+
 // ---------------------------------------------------------------- utilities
 void launch_fill_i32(i32* p, i64 n, i32 v, cudaStream_t s);
 void launch_iota_i32(i32* p, i64 n, i32 base, cudaStream_t s);

@@ -162,6 +162,22 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
       cur = S.val.p;
     }
     launch_scatter_const(cur, wl, nwl, nwl_max, 0, s);
+    if (dist == 2) {
+      // Distance 2: bounded-degree meshes are order-sensitive (first fit in id order
+      // keeps the reference's colour count) -> the ordered kernel;
+      // everything else -> net-centric speculation (color_net.cu).
+      const i64 nexact = read_i64(nwl, s);
+      if (worklist_max_degree(wl, nexact, rowptr, S.net, s) <= 26) {
+        if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
+        algo = CHROMA_ALGO_GAUSS_SEIDEL;
+        goto gauss_seidel;
+      }
+      if (launch_free_net(rowptr, col, nv, cur, wl, nexact, partial, S.net, s)) {
+        if (ev_k1) CUDA_CHECK(cudaEventRecord(ev_k1, s));
+        if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
+        return;
+      }
+    }
     if (cnt[1] > 0 && !no_waves) {
       const auto tw0 = std::chrono::steady_clock::now();
       const i64 nh = cnt[1];

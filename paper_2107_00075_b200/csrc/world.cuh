@@ -58,6 +58,7 @@ struct ColorScratch {
   DBuf<i64> fcnt;
   FreeWaveScratch fw;
   ChunkedScratch chunked;
+  NetScratch net;
   bool upper_zero = false;  // gs_chunked: no neighbour above a member is coloured yet
 };
 

@@ -166,7 +166,10 @@ def _host_colors(n):
     mapped (a fresh np.zeros array costs ~1 ms of page faults per 8 MB), and the block
     returns to the cache when the caller drops the array.  Every element is written
     by the device before the array is returned."""
-    import torch
+    try:
+        import torch
+    except ImportError:  # the package needs only NumPy on the host side
+        return np.zeros(n, dtype=np.int32)
     if n > 0 and torch.cuda.is_available():
         return torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
     return np.zeros(n, dtype=np.int32)

@@ -1,0 +1,107 @@
+"""Parity at the BASELINE configurations' full sizes (BASELINE.json configs C1-C5).
+
+The expected values come from tests/golden/scale.json, written by
+oracle/gen_scale_golden.py from the C oracle (pinned to the reference's own outputs by
+tests/test_oracle_golden.py) on the identical CSR arrays -- the device generators'
+arrays are checked against the oracle generator's by sha256 first.
+  * deterministic mode: sha256 of the int32 colour array, rounds and per-round
+    conflicts, bit-exact (integer path);
+  * free-running mode: a proper colouring (GPU checker) with at most 5 % more colours
+    than the oracle's deterministic run at the same P (north_star).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2107_00075_b200 import graph as G
+from paper_2107_00075_b200 import partition as PT
+from paper_2107_00075_b200 import protocol as R
+from paper_2107_00075_b200 import runtime as RT
+from paper_2107_00075_b200 import verify as V
+from tests.common import sha
+
+pytestmark = pytest.mark.gpu
+
+with open(os.path.join(os.path.dirname(__file__), "golden", "scale.json")) as _fh:
+    SCALE = json.load(_fh)
+
+_CACHE = {}
+
+
+def graph(key):
+    """Device-generated graph of a golden key (cached for the session)."""
+    if key not in _CACHE:
+        _CACHE.clear()
+        build = {
+            "c1_1000": lambda: G.gen_hex_mesh_device(1000, 1000, 1, "cuda"),
+            "c2_128": lambda: G.gen_stencil27(128, device="cuda"),
+            "c3_s24": lambda: G.gen_rmat(24, 16, 1, device="cuda"),
+            "c4_200": lambda: G.gen_hex_mesh_device(200, 200, 200, "cuda"),
+            "c5_2p20": lambda: G.gen_random_bipartite(1 << 20, 32, 3, device="cuda").graph,
+            "c5_2p22": lambda: G.gen_random_bipartite(1 << 22, 32, 3, device="cuda").graph,
+        }[key]
+        _CACHE[key] = build()
+    return _CACHE[key]
+
+
+def run(g, mode, P, algorithm=None):
+    pm = PT.partition_block(g, P)
+    w = RT.build_local_graphs(g, pm, R.ghost_layers_for(R.Mode(mode)))
+    cfg = R.AlgorithmConfig(mode=R.Mode(mode), deterministic=algorithm is None, algorithm=algorithm)
+    colors, reports = R.run_distributed(w, cfg)
+    del w
+    return np.asarray(colors), reports
+
+
+def violations(g, colors, mode):
+    vm = {"d1": "d1", "d1-2gl": "d1", "d2": "d2", "pd2": "pd2"}[mode]
+    mask = None
+    if mode == "pd2":
+        mask = np.zeros(g.num_vertices, np.uint8)
+        mask[: g.num_vertices // 2] = 1
+    return V.count_violations(g, colors, vm, mask)
+
+
+DET = [(k, run_key) for k in sorted(SCALE) for run_key in sorted(SCALE[k]) if "_p" in run_key]
+
+
+@pytest.mark.parametrize("key", sorted(SCALE))
+def test_device_generator_matches_oracle_generator(key):
+    g = graph(key)
+    assert len(g.col_indices) == SCALE[key]["nnz"]
+    assert sha(g.col_indices, "<i8") == SCALE[key]["col_sha256"]
+    assert sha(g.row_offsets, "<i8") == SCALE[key]["rowptr_sha256"]
+
+
+@pytest.mark.parametrize("key,run_key", DET, ids=[f"{k}-{r}" for k, r in DET])
+def test_deterministic_bit_exact(key, run_key):
+    mode, P = run_key.rsplit("_p", 1)
+    ref = SCALE[key][run_key]
+    if mode == "pd2" and key == "c5_2p22":
+        pytest.skip("deterministic PD2 at 2^22 is checked at 2^20 (c5_2p20); 2^22 runs free-mode below")
+    g = graph(key)
+    colors, reports = run(g, mode, int(P))
+    assert sha(colors) == ref["sha256"]
+    assert len(reports) == ref["rounds"]
+    assert [r.conflicts for r in reports] == ref["conflicts"]
+    assert violations(g, colors, mode) == 0
+
+
+FREE = [("c3_s24", "d1", 1), ("c3_s24", "d1", 8), ("c4_200", "d2", 8), ("c4_200", "d2", 1),
+        ("c5_2p22", "pd2", 1), ("c5_2p22", "pd2", 8)]
+
+
+@pytest.mark.parametrize("key,mode,P", FREE, ids=[f"{k}-{m}-P{p}" for k, m, p in FREE])
+def test_free_running_within_5pct(key, mode, P):
+    ref = SCALE.get(key, {}).get(f"{mode}_p{P}")
+    if ref is None:
+        pytest.skip("no oracle value for this configuration")
+    g = graph(key)
+    colors, reports = run(g, mode, P, algorithm="free")
+    assert colors.min() >= 1
+    assert reports[-1].conflicts == 0
+    assert violations(g, colors, mode) == 0
+    ncol = len(np.unique(colors))
+    assert ncol <= 1.05 * ref["colors"], (ncol, ref["colors"])
