@@ -238,20 +238,40 @@ __global__ void k_fill(const i32* lgids, i64 nl, i64 oc, i64 l1, int gl, const i
       }
       continue;
     }
-    for (uint8_t c = 1; c <= 3; c++) {
+    // long row: count the kept owned / layer-1 entries, then place all three classes
+    // in one more pass (rows of a world without ghosts keep every entry in order)
+    i64 n1 = re - rs, n2 = 0;
+    if (nl != oc) {
+      n1 = 0;
       for (i64 e0 = rs; e0 < re; e0 += 32) {
         const i64 e = e0 + lane;
-        bool k = false;
-        i32 u = 0;
-        if (e < re) {
-          u = gcol[e];
-          const uint8_t cu = cls[u];
-          k = cu == c && keep_nbr(lid, oc, l1, gl, cu);
-        }
-        const unsigned b = __ballot_sync(FULL, k);
-        if (k) lcol[pos + __popc(b & lanemask_lt())] = lid_of[u];
-        pos += __popc(b);
+        uint8_t cu = 0;
+        if (e < re) cu = cls[gcol[e]];
+        const bool k = cu >= 1 && cu <= 3 && keep_nbr(lid, oc, l1, gl, cu);
+        n1 += __popc(__ballot_sync(FULL, k && cu == 1));
+        n2 += __popc(__ballot_sync(FULL, k && cu == 2));
       }
+    }
+    i64 p1 = pos, p2 = pos + n1, p3 = pos + n1 + n2;
+    for (i64 e0 = rs; e0 < re; e0 += 32) {
+      const i64 e = e0 + lane;
+      i32 u = 0;
+      uint8_t cu = 0;
+      if (e < re) {
+        u = gcol[e];
+        cu = cls[u];
+      }
+      const bool k = cu >= 1 && cu <= 3 && keep_nbr(lid, oc, l1, gl, cu);
+      const unsigned b1 = __ballot_sync(FULL, k && cu == 1), b2 = __ballot_sync(FULL, k && cu == 2),
+                     b3 = __ballot_sync(FULL, k && cu == 3);
+      if (k) {
+        const unsigned lt = lanemask_lt();
+        const i64 at = cu == 1 ? p1 + __popc(b1 & lt) : cu == 2 ? p2 + __popc(b2 & lt) : p3 + __popc(b3 & lt);
+        lcol[at] = lid_of[u];
+      }
+      p1 += __popc(b1);
+      p2 += __popc(b2);
+      p3 += __popc(b3);
     }
   }
 }
@@ -288,15 +308,23 @@ __global__ void k_bound1(const i64* lrow, const i32* lcol, i64 nl, i64 oc, uint8
 }
 
 // boundary_d2 = boundary_d1 u owned vertices with an owned boundary_d1 neighbour
+// a warp per owned row: lanes test 32 owned neighbours at a time, stop at the first
+// boundary_d1 one (rows are lid-sorted: owned neighbours form a prefix)
 __global__ void k_bound2(const i64* lrow, const i32* lcol, i64 oc, const uint8_t* b1, uint8_t* b2) {
-  for (i64 v = blockIdx.x * (i64)blockDim.x + threadIdx.x; v < oc; v += (i64)gridDim.x * blockDim.x) {
-    uint8_t f = b1[v];
-    for (i64 e = lrow[v]; !f && e < lrow[v + 1]; e++) {
-      const i32 u = lcol[e];
-      if (u >= oc) break;
-      f = b1[u];
+  const int lane = threadIdx.x & 31;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 v = warp; v < oc; v += nwarps) {
+    bool f = b1[v] != 0;
+    const i64 re = lrow[v + 1];
+    for (i64 e0 = lrow[v]; !f && e0 < re; e0 += 32) {
+      const i64 e = e0 + lane;
+      const i32 u = e < re ? lcol[e] : (i32)oc;
+      const bool hit = u < oc && b1[u];
+      f = __any_sync(FULL, hit);
+      if (__any_sync(FULL, u >= oc)) break;
     }
-    b2[v] = f;
+    if (lane == 0) b2[v] = f ? 1 : 0;
   }
 }
 
@@ -585,7 +613,8 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       ecount.zero(s);
       k_bound1<<<G(nl), 256, 0, s>>>(T.lrow.p, T.lcol.p, nl, oc, b1f.p, ecount.p);
       count_launch();
-      k_bound2<<<G(oc), 256, 0, s>>>(T.lrow.p, T.lcol.p, oc, b1f.p, b2f.p);
+      if (nl > oc) k_bound2<<<GW(oc), 256, 0, s>>>(T.lrow.p, T.lcol.p, oc, b1f.p, b2f.p);
+      else CUDA_CHECK(cudaMemsetAsync(b2f.p, 0, oc + 1, s));  // no ghosts: no boundary
       count_launch();
       T.b1.alloc(oc + 1, s);
       T.b2.alloc(oc + 1, s);
