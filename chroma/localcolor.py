@@ -1,0 +1,12 @@
+"""Drop-in module path: `chroma.localcolor` -> paper_2107_00075_b200.localcolor (the B200 backend).
+
+Reference: /root/reference/pkg/src/chroma/localcolor.py.  Existing code that imports the
+reference package keeps working unchanged with this repository on its path."""
+from paper_2107_00075_b200 import localcolor as _impl
+from paper_2107_00075_b200.localcolor import *  # noqa: F401,F403
+
+__all__ = list(getattr(_impl, "__all__", []))
+
+
+def __getattr__(name):
+    return getattr(_impl, name)

@@ -133,6 +133,10 @@ typedef struct chroma_comm chroma_comm;   /* an NCCL communicator (one per proce
 int chroma_nccl_unique_id(void* id_out_128);
 int chroma_comm_create(const void* nccl_id_128, int32_t nranks, int32_t rank, int device,
                        chroma_comm** out);
+/* One process driving ndev GPUs (rank i on devices[i]): ncclCommInitAll; out[i] is
+ * rank i's communicator.  Each rank's world must then be connected and run from its
+ * own host thread (the calls are collective). */
+int chroma_comm_create_all(int32_t ndev, const int* devices, chroma_comm** out);
 int chroma_comm_destroy(chroma_comm* c);
 /* The world borrows `comm` (which must outlive it). */
 int chroma_world_connect(chroma_world* w, chroma_comm* comm, int32_t nranks, int32_t rank,

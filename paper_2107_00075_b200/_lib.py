@@ -60,6 +60,7 @@ def lib():
         "chroma_nccl_unique_id": (I, [P]),
         "chroma_comm_create": (I, [P, i32, i32, I, C.POINTER(P)]),
         "chroma_comm_destroy": (I, [P]),
+        "chroma_comm_create_all": (I, [i32, P, P]),
         "chroma_world_connect": (I, [P, P, i32, i32, P, P, P, P]),
         "chroma_world_global_degrees": (I, [P, i32, P]),
         "chroma_world_reset_exchange": (I, [P]),
@@ -91,7 +92,20 @@ EXPORTS = ("chroma_last_error", "chroma_version", "chroma_device_count", "chroma
            "chroma_world_connect", "chroma_world_global_degrees", "chroma_world_reset_exchange",
            "chroma_world_exchange", "chroma_world_color", "chroma_world_detect",
            "chroma_run_distributed", "chroma_world_colors_device", "chroma_world_last_timing",
-           "chroma_launch_count", "chroma_gen_rmat", "chroma_gen_random_bipartite", "chroma_gen_box")
+           "chroma_launch_count", "chroma_gen_rmat", "chroma_gen_random_bipartite", "chroma_gen_box",
+           "chroma_comm_create_all")
+
+
+def error_for(status: int, msg: str) -> Exception:
+    """The reference's exception class for a status code."""
+    if status == EVALUE:
+        return ValueError(msg)
+    if status == EPROTOCOL:
+        from .runtime import ProtocolError
+        return ProtocolError(msg)
+    if status == ERUNTIME:
+        return RuntimeError(msg)
+    return RuntimeError(f"CUDA failure ({status}): {msg}")
 
 
 def check(status: int, what: str = "") -> None:
@@ -101,14 +115,7 @@ def check(status: int, what: str = "") -> None:
     msg = lib().chroma_last_error().decode(errors="replace")
     if what:
         msg = f"{what}: {msg}"
-    if status == EVALUE:
-        raise ValueError(msg)
-    if status == EPROTOCOL:
-        from .runtime import ProtocolError
-        raise ProtocolError(msg)
-    if status == ERUNTIME:
-        raise RuntimeError(msg)
-    raise RuntimeError(f"CUDA failure ({status}): {msg}")
+    raise error_for(status, msg)
 
 
 def ptr(a: np.ndarray):

@@ -411,6 +411,27 @@ int chroma_comm_create(const void* id_bytes, int32_t nranks, int32_t rank, int d
   });
 }
 
+int chroma_comm_create_all(int32_t ndev, const int* devices, chroma_comm** out) {
+  return guarded([&] {
+#ifdef CHROMA_WITH_NCCL
+    CHROMA_REQUIRE(ndev >= 1, CHROMA_EVALUE, "ndev must be >= 1");
+    std::vector<ncclComm_t> comms((size_t)ndev);
+    ncclResult_t r = ncclCommInitAll(comms.data(), ndev, devices);
+    if (r != ncclSuccess) throw Error(CHROMA_ECUDA, std::string("ncclCommInitAll: ") + ncclGetErrorString(r));
+    for (int i = 0; i < ndev; i++) {
+      auto* c = new chroma_comm();
+      c->comm = comms[(size_t)i];
+      c->nranks = ndev;
+      c->rank = i;
+      out[i] = c;
+    }
+#else
+    (void)ndev; (void)devices; (void)out;
+    throw Error(CHROMA_ECUDA, "built without NCCL");
+#endif
+  });
+}
+
 int chroma_comm_destroy(chroma_comm* c) {
   return guarded([&] {
 #ifdef CHROMA_WITH_NCCL

@@ -487,10 +487,12 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
     a.trace = tbuf.p;
   }
   const size_t dsmem = sizeof(u32) * CF_WORDS * CF_THREADS;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};  // per device
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
     CUDA_CHECK(cudaFuncSetAttribute((void*)k_gs_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_gs_chunked, grid, CF_THREADS, args, dsmem, s));
   count_launch();

@@ -104,11 +104,20 @@ void launch_clamp_nonneg(i32* dst, const i32* src, i64 n, cudaStream_t s) {
   count_launch();
 }
 
-// Scratch for cub temporaries (grow-only, per thread of control; intentionally
-// never destroyed so no free runs after the CUDA context is gone).
+// Scratch (grow-only, per host thread AND device -- one process may drive several
+// GPUs from a thread pool; intentionally never destroyed so no free runs after the
+// CUDA context is gone).
+template <typename T>
+static DBuf<T>& per_device_scratch(DBuf<T>* (&slots)[64]) {
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) d = 0;
+  if (!slots[d]) slots[d] = new DBuf<T>();
+  return *slots[d];
+}
 static DBuf<uint8_t>& cub_tmp() {
-  static thread_local DBuf<uint8_t>* b = new DBuf<uint8_t>();
-  return *b;
+  static thread_local DBuf<uint8_t>* b[64] = {};
+  return per_device_scratch(b);
 }
 #define t_cub_tmp cub_tmp()
 
@@ -153,7 +162,8 @@ void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* 
 
 void sort_i32(i32* keys, i64 n, cudaStream_t s) {
   if (n <= 1) return;
-  static thread_local DBuf<i32>* alt = new DBuf<i32>();
+  static thread_local DBuf<i32>* alts[64] = {};
+  DBuf<i32>* alt = &per_device_scratch(alts);
   alt->reserve(n, s);
   cub::DoubleBuffer<i32> db(keys, alt->p);
   size_t bytes = 0;
@@ -167,7 +177,8 @@ void sort_i32(i32* keys, i64 n, cudaStream_t s) {
 
 void sort_u64(u64* keys, i64 n, cudaStream_t s) {
   if (n <= 1) return;
-  static thread_local DBuf<u64>* alt = new DBuf<u64>();
+  static thread_local DBuf<u64>* alts[64] = {};
+  DBuf<u64>* alt = &per_device_scratch(alts);
   alt->reserve(n, s);
   cub::DoubleBuffer<u64> db(keys, alt->p);
   size_t bytes = 0;

@@ -146,7 +146,7 @@ def compute_global_degrees(world: RankWorld) -> list:
     out = []
     for lg in world.local_graphs:
         d = np.zeros(lg.num_local, dtype=np.int64)
-        _lib.check(_lib.lib().chroma_world_global_degrees(world.handle.h, lg.rank, _lib.ptr(d)))
+        _lib.check(_lib.lib().chroma_world_global_degrees(lg._wh.h, lg.rank, _lib.ptr(d)))
         lg.global_degrees = d
         out.append(d)
     return out
@@ -196,6 +196,20 @@ def run_distributed(world, cfg: AlgorithmConfig, out=None):
     rec = np.zeros((cap, P), dtype=np.int64)
     nrep = C.c_int64(0)
     n_out = world.output_length() if hasattr(world, "output_length") else world.num_global_vertices
+    if hasattr(world, "run") and hasattr(world, "devices"):  # MultiDeviceWorld
+        colors, st, rep, rec, nr = world.run(_lib.MODE[mode.value], bool(cfg.recolor_degrees), cfg.algo_code(),
+                                             int(cfg.max_rounds))
+        reports = _reports_from(rep, rec, nr, P)
+        world.total_bytes = sum(r.bytes_sent for r in reports)
+        world.total_messages = sum(r.messages_sent for r in reports)
+        if st == _lib.ENONCONV:
+            raise NonConvergenceError(f"no convergence after {cfg.max_rounds} rounds", reports)
+        _lib.check(st, "run_distributed")
+        if out is not None:
+            import torch
+            out.copy_(torch.from_numpy(colors))
+            return out, reports
+        return colors, reports
     if out is not None:
         if (not getattr(out, "is_cuda", False) or str(out.dtype) != "torch.int32" or not out.is_contiguous()
                 or out.numel() != n_out):

@@ -211,8 +211,18 @@ def build_local_graphs(g, pm: PartitionMap, ghost_layers: int = 1) -> RankWorld:
         raise ValueError("num_ranks must be >= 1")
     if len(pm.owner) != g.num_vertices:
         raise ValueError("partition size does not match graph")
+    # one process, several GPUs: rank r on its own device (multidev.py)
+    from .multidev import MultiDeviceWorld, devices_for
+    devs = devices_for(pm.num_ranks)
+    if devs is not None:
+        return MultiDeviceWorld(g, pm, ghost_layers, devs)
+    return _build_virtual(g, pm, ghost_layers)
+
+
+def _build_virtual(g, pm: PartitionMap, ghost_layers: int, device: int | None = None) -> RankWorld:
+    """Every rank on one device ("virtual ranks"; the halo is a device copy)."""
     # owner range / empty-rank validation (PartitionMap.validate) runs on the device
-    wh = WorldHandle(g, pm, ghost_layers, 0, pm.num_ranks)
+    wh = WorldHandle(g, pm, ghost_layers, 0, pm.num_ranks, device)
     lgs = [LocalGraph(wh, r, ghost_layers) for r in range(pm.num_ranks)]
     world = RankWorld(num_ranks=pm.num_ranks, ghost_layers=ghost_layers, local_graphs=lgs,
                       partition=pm, num_global_vertices=g.num_vertices, source_stats=device_stats(wh),
@@ -224,6 +234,11 @@ def build_local_graphs(g, pm: PartitionMap, ghost_layers: int = 1) -> RankWorld:
 def exchange_boundary_colors(world: RankWorld, colorings: list, changed_only: bool = False):
     """Owner -> every ghost copy, changed-only against the last broadcast
     (chroma/runtime.py:271-308).  Returns (bytes_sent, messages_sent)."""
+    if hasattr(world, "virtual_world"):  # MultiDeviceWorld: the virtual copy keeps the state
+        b, m = exchange_boundary_colors(world.virtual_world(), colorings, changed_only)
+        world.total_bytes += b
+        world.total_messages += m
+        return b, m
     if world.handle is None:
         raise ValueError("world was not built by paper_2107_00075_b200.runtime.build_local_graphs")
     bufs = [np.ascontiguousarray(c, dtype=np.int32) for c in colorings]

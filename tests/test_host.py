@@ -169,3 +169,15 @@ def test_no_cpu_fallback():
         RT.build_local_graphs(g, PT.partition_block(g, 2), 1)
     with pytest.raises(RuntimeError):
         V.verify_d1(g, np.ones(30, np.int32))
+
+
+def test_chroma_import_path_is_the_b200_backend():
+    """`from chroma import protocol` (the reference's module paths) resolves to this
+    package (drop-in: callers' imports do not change)."""
+    import importlib
+    import paper_2107_00075_b200 as pkg
+    for m in ("graph", "partition", "runtime", "localcolor", "protocol", "verify"):
+        shim = importlib.import_module(f"chroma.{m}")
+        impl = getattr(pkg, m) if hasattr(pkg, m) else importlib.import_module(f"paper_2107_00075_b200.{m}")
+        for name in getattr(impl, "__all__", []):
+            assert getattr(shim, name) is getattr(impl, name), (m, name)
