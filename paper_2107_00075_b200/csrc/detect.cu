@@ -18,6 +18,10 @@
 #include <cstdlib>
 #include <functional>
 
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/unique.h>
+
 #include "kernels.cuh"
 
 namespace chroma {
@@ -98,6 +102,71 @@ __global__ void k_events(DevDetect a, i64* cnt, const i64* off, int2* ev) {
       }
     }
     if (!WRITE && lane == 0) cnt[i] = count;
+  }
+}
+
+// Distance 1, rows of any length: a warp takes 32 consecutive detection rows; a lane
+// walks its own row when it has at most 32 entries (most ghost rows hold a few
+// back-edges), the warp walks the longer ones together.  Same events, same order.
+template <bool WRITE>
+__global__ void k_events_d1(DevDetect a, i64* cnt, const i64* off, int2* ev) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 b = warp * 32; b < a.nrows; b += nwarps * 32) {
+    const i64 i = b + lane;
+    i32 v = -1, cv = 0;
+    i64 rs = 0, re = 0;
+    if (i < a.nrows && (!WRITE || cnt[i] != 0)) {
+      v = a.rows[i];
+      cv = a.colors[v];
+      if (cv != 0) {
+        rs = a.rowptr[v];
+        re = a.rowptr[v + 1];
+      }
+    }
+    const bool lng = re - rs > 32;
+    if (!lng && re > rs) {
+      i64 pos = WRITE ? off[i] : 0, count = 0;
+      for (i64 e0 = rs; e0 < re; e0 += 8) {
+        i32 xs[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) xs[q] = e0 + q < re ? a.col[e0 + q] : -1;
+        bool hs[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) hs[q] = xs[q] >= 0 && a.colors[xs[q]] == cv;
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          if (hs[q]) {
+            if (WRITE) ev[pos] = make_event(a, v, xs[q]);
+            pos++;
+            count++;
+          }
+      }
+      if (!WRITE) cnt[i] = count;
+    } else if (!lng && !WRITE && i < a.nrows) {
+      cnt[i] = 0;
+    }
+    for (unsigned lm = __ballot_sync(FULL, lng); lm; lm &= lm - 1) {
+      const int src = __ffs(lm) - 1;
+      const i32 vl = __shfl_sync(FULL, v, src), cl = __shfl_sync(FULL, cv, src);
+      const i64 ls = __shfl_sync(FULL, rs, src), le = __shfl_sync(FULL, re, src);
+      i64 pos = WRITE ? off[b + src] : 0, count = 0;
+      for (i64 e0 = ls; e0 < le; e0 += 32) {
+        const i64 e = e0 + lane;
+        i32 x = 0;
+        bool hit = false;
+        if (e < le) {
+          x = a.col[e];
+          hit = a.colors[x] == cl;
+        }
+        const unsigned bb = __ballot_sync(FULL, hit);
+        if (WRITE && hit) ev[pos + __popc(bb & lanemask_lt())] = make_event(a, vl, x);
+        pos += __popc(bb);
+        count += __popc(bb);
+      }
+      if (!WRITE && lane == 0) cnt[b + src] = count;
+    }
   }
 }
 
@@ -211,6 +280,174 @@ __global__ void __launch_bounds__(1024, 1) k_resolve_grid(const int2* ev, i64 E,
   if ((threadIdx.x & 31) == 0 && n) atomicAdd(conflicts, n);
 }
 
+// Changed-side event emission (distance 1, sequential, incremental): an event needs
+// a changed endpoint (see below), and the local CSR is symmetric (owned rows are
+// complete, ghost rows hold the back-edges), so walking the rows of the changed
+// vertices finds every scanned pair (v ghost, x in row(v)) with equal colours:
+// from changed y, (y, x) when y is a ghost, (x, y) when x is.  Keys (v << 32 | x)
+// sorted and de-duplicated are exactly the reference's scan order (ghost rows
+// ascending, each row ascending).  WRITE = false counts.
+constexpr i64 SEG = 256;  // row entries per work item of the changed-side walk
+
+// segments of the long (> 32 entries) source rows; short ones go to k_emit_short
+__global__ void k_changed_nseg(const i64* rowptr, const i32* changed, i64 nch, i64* nseg, bool long_only) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nch; i += (i64)gridDim.x * blockDim.x) {
+    const i32 y = changed[i];
+    const i64 d = rowptr[y + 1] - rowptr[y];
+    nseg[i] = long_only && d <= 32 ? 0 : (d + SEG - 1) / SEG;
+  }
+}
+
+// Short source rows (<= 32 entries), one lane each; keys appended with one atomic
+// per warp.  ROWS: sources are detection rows, emit (y, x); otherwise sources are
+// changed vertices, emit (y, x) if y is a ghost and (x, y) if x is.
+template <bool WRITE, bool ROWS>
+__global__ void k_emit_short(const i64* rowptr, const i32* col, const i32* colors, const uint8_t* owned,
+                             const i32* src, i64 nsrc, unsigned long long* cnt, u64* keys) {
+  const int lane = threadIdx.x & 31;
+  for (i64 b = (blockIdx.x * (i64)blockDim.x + threadIdx.x) - lane; b < nsrc; b += (i64)gridDim.x * blockDim.x) {
+    const i64 i = b + lane;
+    i32 y = -1, cy = 0;
+    i64 rs = 0, re = 0;
+    bool gy = ROWS;
+    if (i < nsrc) {
+      y = src[i];
+      cy = colors[y];
+      rs = rowptr[y];
+      re = rowptr[y + 1];
+      if (!ROWS) gy = !owned[y];
+      if (re - rs > 32 || cy == 0) re = rs;  // long rows: k_changed_events
+    }
+    unsigned k = 0;
+    for (int pass = 0; pass < (WRITE ? 2 : 1); pass++) {
+      unsigned long long at = 0;
+      if (pass == 1) {
+        unsigned inc = k;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned t = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += t;
+        }
+        const unsigned tot = __shfl_sync(FULL, inc, 31);
+        unsigned long long base = 0;
+        if (lane == 31 && tot) base = atomicAdd(cnt, (unsigned long long)tot);
+        base = __shfl_sync(FULL, base, 31);
+        at = base + inc - k;
+      }
+      for (i64 e0 = rs; e0 < re; e0 += 8) {
+        i32 xs[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) xs[q] = e0 + q < re ? col[e0 + q] : -1;
+        bool hs[8], gs[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          hs[q] = xs[q] >= 0 && colors[xs[q]] == cy;
+          gs[q] = !ROWS && hs[q] && !owned[xs[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          if (!hs[q]) continue;
+          if (pass == 0) {
+            k += (gy ? 1u : 0u) + (gs[q] ? 1u : 0u);
+          } else {
+            if (gy) keys[at++] = ((u64)(u32)y << 32) | (u32)xs[q];
+            if (gs[q]) keys[at++] = ((u64)(u32)xs[q] << 32) | (u32)y;
+          }
+        }
+      }
+    }
+    if (!WRITE) {
+      const unsigned tot = __reduce_add_sync(FULL, k);
+      if (lane == 0 && tot) atomicAdd(cnt, (unsigned long long)tot);
+    }
+  }
+}
+
+// A warp per item (changed vertex i, segment of SEG row entries): item j belongs to
+// the last i with segoff[i] <= j.  Keys go to *cnt-indexed slots (one atomic per warp
+// step; the caller sorts them).  WRITE = false only counts.
+template <bool WRITE, bool ROWS>
+__global__ void k_changed_events(const i64* rowptr, const i32* col, const i32* colors, const uint8_t* owned,
+                                 const i32* changed, i64 nch, const i64* segoff, i64 nitems,
+                                 unsigned long long* cnt, u64* keys) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 j = warp; j < nitems; j += nwarps) {
+    // upper_bound(segoff, j) - 1, searched by one lane
+    i64 i = 0;
+    if (lane == 0) {
+      i64 lo = 0, hi = nch;
+      while (hi - lo > 1) {
+        const i64 mid = (lo + hi) >> 1;
+        if (segoff[mid] <= j) lo = mid; else hi = mid;
+      }
+      i = lo;
+    }
+    i = __shfl_sync(FULL, i, 0);
+    const i32 y = changed[i];
+    const i32 cy = colors[y];
+    const bool gy = ROWS || !owned[y];
+    const i64 rs = rowptr[y], re = cy == 0 ? rowptr[y] : rowptr[y + 1];
+    const i64 s0 = rs + (j - segoff[i]) * SEG;
+    const i64 s1 = s0 + SEG < re ? s0 + SEG : re;
+    unsigned long long mine = 0;
+    for (i64 e0 = s0; e0 < s1; e0 += 32) {
+      const i64 e = e0 + lane;
+      i32 x = 0;
+      unsigned k = 0;
+      bool gx = false;
+      if (e < s1) {
+        x = col[e];
+        if (colors[x] == cy) {
+          gx = !ROWS && !owned[x];
+          k = (gy ? 1u : 0u) + (gx ? 1u : 0u);
+        }
+      }
+      if (!WRITE) {
+        mine += k;
+        continue;
+      }
+      unsigned inc = k;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const unsigned tot = __shfl_sync(FULL, inc, 31);
+      unsigned long long base = 0;
+      if (tot) {
+        if (lane == 31) base = atomicAdd(cnt, (unsigned long long)tot);
+        base = __shfl_sync(FULL, base, 31);
+      }
+      if (k) {
+        unsigned long long at = base + inc - k;
+        if (gy) keys[at++] = ((u64)(u32)y << 32) | (u32)x;
+        if (gx) keys[at] = ((u64)(u32)x << 32) | (u32)y;
+      }
+    }
+    if (!WRITE) {
+      mine = __reduce_add_sync(FULL, (unsigned)mine);
+      if (lane == 0 && mine) atomicAdd(cnt, mine);
+    }
+  }
+}
+
+__global__ void k_flag_changed(const i32* colors, const i32* prev, i64 n, uint8_t* flag) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 c = colors[i];
+    flag[i] = (c != 0 && c != prev[i]) ? 1 : 0;
+  }
+}
+
+// unique sorted keys -> events in scan order, loser by the cascade
+__global__ void k_keys_to_events(DevDetect a, const u64* keys, i64 k, int2* ev) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < k; i += (i64)gridDim.x * blockDim.x) {
+    const u64 key = keys[i];
+    ev[i] = make_event(a, (i32)(key >> 32), (i32)(key & 0xffffffffu));
+  }
+}
+
 // Incremental detection: an event (equal non-zero colours on a scanned pair) can
 // only exist if one endpoint changed colour since the previous detection (which
 // left no conflicting pair behind, and unchanged pairs keep their colours).  Mark
@@ -228,6 +465,14 @@ __global__ void k_mark_changed(const i64* rowptr, const i32* col, const i32* col
     if (i < n) {
       const i32 c = colors[i];
       ch = c != 0 && c != prev[i];
+    }
+    if (DIST == 1 && ch) {  // short rows: the lane marks its own row
+      const i64 rs = rowptr[i], re = rowptr[i + 1];
+      if (re - rs <= 32) {
+        mark[i] = 1;
+        for (i64 e = rs; e < re; e++) mark[col[e]] = 1;
+        ch = false;
+      }
     }
     unsigned m = __ballot_sync(FULL, ch);
     while (m) {
@@ -490,6 +735,65 @@ void run_detect_free_lists(const DetectArgs& A, i64 nv, const FreeList* lists, i
   CUDA_CHECK(cudaGetLastError());
 }
 
+static void resolve_events(const DetectArgs& A, DetectScratch& S, i64 E, unsigned long long* conflicts_dev,
+                           i64 num_vertices, cudaStream_t s);
+
+// Keyed D1 event emission from `src` (detection rows, or changed vertices): short
+// rows by lanes, long rows in SEG-entry segments by warps; returns E, the events in
+// S.ev in scan order.
+static i64 keyed_events(const DetectArgs& A, const DevDetect& a, DetectScratch& S, const i32* src, i64 nsrc,
+                        bool rows_mode, cudaStream_t s) {
+  S.cnt.reserve(nsrc, s);
+  S.off.reserve(nsrc, s);
+  S.total.reserve(1, s);
+  S.nch.reserve(1, s);
+  // rows mode: short rows by lanes (k_emit_short), long ones in segments; changed
+  // mode: every row in segments (changed vertices are few and their rows long)
+  k_changed_nseg<<<grid_for(nsrc, 256, num_sms() * 16), 256, 0, s>>>(A.rowptr, src, nsrc, S.cnt.p, rows_mode);
+  count_launch();
+  exclusive_scan_i64(S.cnt.p, S.off.p, nsrc, s);
+  k_total<<<1, 1, 0, s>>>(S.cnt.p, S.off.p, nsrc, S.total.p);
+  count_launch();
+  CUDA_CHECK(cudaMemsetAsync(S.nch.p, 0, sizeof(unsigned long long), s));
+  i64 nitems = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&nitems, S.total.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  const int gs = grid_for(nsrc, 256, num_sms() * 16);
+  const int gw = grid_for(std::max<i64>(nitems, 1) * 32, 256, num_sms() * 16);
+  auto emit = [&](auto write, u64* keys) {
+    constexpr bool W = decltype(write)::value;
+    if (rows_mode) {
+      k_emit_short<W, true><<<gs, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.nch.p, keys);
+      if (nitems)
+        k_changed_events<W, true><<<gw, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.off.p,
+                                                     nitems, S.nch.p, keys);
+      count_launch(nitems ? 2 : 1);
+    } else {
+      if (nitems)
+        k_changed_events<W, false><<<gw, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.off.p,
+                                                      nitems, S.nch.p, keys);
+      count_launch();
+    }
+  };
+  emit(std::false_type{}, nullptr);
+  unsigned long long nku = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&nku, S.nch.p, sizeof(nku), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  const i64 nk = (i64)nku;
+  if (nk == 0) return 0;
+  S.keys.reserve(nk, s);
+  CUDA_CHECK(cudaMemsetAsync(S.nch.p, 0, sizeof(unsigned long long), s));
+  emit(std::true_type{}, S.keys.p);
+  sort_u64(S.keys.p, nk, s);
+  S.ukeys.reserve(nk, s);
+  const i64 E = unique_u64(S.keys.p, nk, S.ukeys.p, s);
+  CHROMA_REQUIRE(E < INT32_MAX, CHROMA_ERUNTIME, "too many conflict events");
+  S.ev.reserve(E, s);
+  k_keys_to_events<<<grid_for(E, 256, num_sms() * 16), 256, 0, s>>>(a, S.ukeys.p, E, S.ev.p);
+  count_launch();
+  return E;
+}
+
 void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
                 unsigned long long* conflicts_dev, cudaStream_t s) {
   if (A.nrows <= 0) return;
@@ -529,6 +833,35 @@ void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
     CUDA_CHECK(cudaMemcpyAsync(S.prev.p, A.colors, sizeof(i32) * num_vertices, cudaMemcpyDeviceToDevice, s));
     S.prev_valid = true;
   };
+  static const bool no_keyed = std::getenv("CHROMA_DETECT_ROWSCAN") != nullptr;
+  if (A.dist == 1 && A.owned_flag && A.sequential && !no_keyed) {
+    // keyed emission: every equal-coloured scanned pair as a key (v << 32 | x),
+    // sorted and de-duplicated into the reference's scan order
+    const i32* src = A.rows;
+    i64 nsrc = A.nrows;
+    bool rows_mode = true;
+    if (A.incremental && S.prev_valid) {
+      // only rows around changed vertices can hold an event: walk from the changed side
+      S.mark.reserve(num_vertices, s);
+      k_flag_changed<<<grid_for(num_vertices, 256, num_sms() * 16), 256, 0, s>>>(A.colors, S.prev.p, num_vertices,
+                                                                                 S.mark.p);
+      count_launch();
+      S.chl.reserve(num_vertices, s);
+      S.narows.reserve(1, s);
+      select_flagged(S.mark.p, num_vertices, S.chl.p, S.narows.p, s);
+      CUDA_CHECK(cudaMemcpyAsync(&nsrc, S.narows.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      src = S.chl.p;
+      rows_mode = false;
+    }
+    mark_t();
+    const i64 E = nsrc > 0 ? keyed_events(A, a, S, src, nsrc, rows_mode, s) : 0;
+    mark_t();
+    if (E > 0) resolve_events(A, S, E, conflicts_dev, num_vertices, s);
+    mark_t();
+    save_prev();
+    return;
+  }
   if (A.incremental && S.prev_valid) {
     S.mark.reserve(num_vertices, s);
     CUDA_CHECK(cudaMemsetAsync(S.mark.p, 0, num_vertices, s));
@@ -558,7 +891,7 @@ void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
   const int g = grid_for(nrows * 32, 256, num_sms() * 16);
   auto launch = [&](auto wr) {
     constexpr bool W = decltype(wr)::value;
-    if (A.dist == 1) k_events<1, false, W><<<g, 256, 0, s>>>(a, S.cnt.p, S.off.p, S.ev.p);
+    if (A.dist == 1) k_events_d1<W><<<grid_for(nrows, 256, num_sms() * 16), 256, 0, s>>>(a, S.cnt.p, S.off.p, S.ev.p);
     else if (A.partial) k_events<2, true, W><<<g, 256, 0, s>>>(a, S.cnt.p, S.off.p, S.ev.p);
     else k_events<2, false, W><<<g, 256, 0, s>>>(a, S.cnt.p, S.off.p, S.ev.p);
     count_launch();
@@ -580,6 +913,16 @@ void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
   S.ev.reserve(E, s);
   launch(std::true_type{});
   mark_t();
+  resolve_events(A, S, E, conflicts_dev, num_vertices, s);
+  mark_t();
+  save_prev();
+  mark_t();
+}
+
+// Resolve E ordered events in S.ev (fixed point over the event order, F5) and
+// uncolour the fired losers; adds the number fired to *conflicts_dev.
+static void resolve_events(const DetectArgs& A, DetectScratch& S, i64 E, unsigned long long* conflicts_dev,
+                           i64 num_vertices, cudaStream_t s) {
   S.fired.reserve(E, s);
   S.kill.reserve(num_vertices, s);
   if (A.sequential && E > 32768) {
@@ -599,9 +942,6 @@ void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
   }
   count_launch();
   CUDA_CHECK(cudaGetLastError());
-  mark_t();
-  save_prev();
-  mark_t();
 }
 
 }  // namespace chroma

@@ -43,7 +43,9 @@ constexpr int CF_WARPS = CF_THREADS / 32;
 constexpr int CF_WORDS = 32;          // bitmap of colours 1..1024
 constexpr i64 CF_TINY = 32;           // rows up to this length: one lane
 constexpr i64 CF_HEAVY = 4096;        // rows longer than this: one CTA
-constexpr int CF_HDR = 4;             // pool record: [k0, k1, nw, 0 | bitmap words]
+constexpr int CF_HDR = 4;             // pool record: [k0, k1, nw, nopen | bitmap words | open lids]
+constexpr int CF_OPEN = 128;          // open intra members listed per long row (more: walk the segment)
+constexpr u32 OPEN_WALK = 0xffffffffu;
 constexpr unsigned FULLM = 0xffffffffu;
 constexpr int CF_HUBW = 2;            // warps per CTA that resolve open hub rows
 constexpr int CF_HUBMAX = 16;         // hubs of one chunk per hub warp
@@ -134,6 +136,7 @@ __device__ void first_lane(const CfArgs& a, i32 v, i32 s0) {
   r[0] = (u32)nlt0;
   r[1] = (u32)nltv;
   r[2] = 2;
+  r[3] = OPEN_WALK;  // a short row: the resolver walks its (<= 32-entry) segment
   r[4] = (u32)m;
   r[5] = (u32)(m >> 32);
   a.desc[v] = off;
@@ -145,7 +148,7 @@ struct RowScan {
 // a row scanned by `nthreads` cooperating threads (a warp, or a CTA when cta) into
 // the shared bitmap bm; stops after the step that reached entries above v
 __device__ void first_scan(const CfArgs& a, i32 v, i32 s0, int tid, int nthreads, bool cta, u32* bm,
-                           RowScan& out) {
+                           RowScan& out, i32* olist, int* on) {
   const i64 rs = a.rowptr[v], re = a.rowptr[v + 1];
   int intra = 0, nlt0 = 0, nltv = 0;
   for (i64 j = rs; j < re; j += (i64)nthreads * 4) {
@@ -169,6 +172,10 @@ __device__ void first_scan(const CfArgs& a, i32 v, i32 s0, int tid, int nthreads
       intra += open;
       nlt0 += u < s0;
       nltv += u < v;
+      if (open) {  // list it (the resolver then waits on these entries only)
+        const int k = atomicAdd(on, 1);
+        if (k < CF_OPEN) olist[k] = u;
+      }
       if (c >= 1 && c <= CF_WORDS * 32) atomicOr(bm + ((c - 1) >> 5), 1u << ((c - 1) & 31));
     }
     const bool any = cta ? __syncthreads_or(above) : __any_sync(FULLM, above);
@@ -188,7 +195,8 @@ __device__ __forceinline__ i32 warp_mex(const u32* bm, int lane) {
 }
 
 // finish a cooperative first pass (one warp)
-__device__ void first_finish(const CfArgs& a, i32 v, const RowScan& r, const u32* bm, int lane) {
+__device__ void first_finish(const CfArgs& a, i32 v, const RowScan& r, const u32* bm, int lane, const i32* olist,
+                             int nopen) {
   const i32 t = warp_mex(bm, lane);
   if (t == 0) {  // more than 1024 colours: publish anything (no waiter may hang), fall back
     if (lane == 0) {
@@ -202,17 +210,21 @@ __device__ void first_finish(const CfArgs& a, i32 v, const RowScan& r, const u32
     return;
   }
   const int nw = words_for(a.rowptr[v + 1] - a.rowptr[v]);
+  const bool listed = nopen <= CF_OPEN;
   u32 off = 0;
   if (lane == 0) {
-    off = pool_alloc(a, nw);
+    off = pool_alloc(a, nw + (listed ? nopen : 0));
     u32* rec = a.pool + off;
     rec[0] = (u32)r.nlt0;
     rec[1] = (u32)r.nltv;
     rec[2] = (u32)nw;
+    rec[3] = listed ? (u32)nopen : OPEN_WALK;
     a.desc[v] = off;
   }
   off = __shfl_sync(FULLM, off, 0);
   if (lane < nw) a.pool[off + CF_HDR + lane] = bm[lane];
+  if (listed)
+    for (int k = lane; k < nopen; k += 32) a.pool[off + CF_HDR + nw + k] = (u32)olist[k];
 }
 
 // ------------------------------------------------------------------ dataflow
@@ -234,9 +246,16 @@ __device__ void resolve_lane(const CfArgs& a, i32 v, u32* lbm) {
   const i64 rs = a.rowptr[v];
   const i64 k0 = rs + __ldcg(rec), k1 = rs + __ldcg(rec + 1);
   const int nw = (int)__ldcg(rec + 2);
+  const u32 nopen = __ldcg(rec + 3);
 #pragma unroll 4
   for (int w = 0; w < CF_WORDS; w++) lbm[w * CF_THREADS] = w < nw ? __ldcg(rec + CF_HDR + w) : 0u;
-  for (i64 j = k0; j < k1; j += 8) {
+  const bool listed = nopen != OPEN_WALK && a.rowptr[v + 1] - rs > CF_TINY;
+  for (u32 k = 0; listed && k < nopen; k++) {
+    const i32 x = wait_final(a, (i32)__ldcg(rec + CF_HDR + nw + k));
+    const i32 c = -x - 2;
+    if (c >= 1 && c <= CF_WORDS * 32) lbm[((c - 1) >> 5) * CF_THREADS] |= 1u << ((c - 1) & 31);
+  }
+  for (i64 j = listed ? k1 : k0; j < k1; j += 8) {
     i32 us[8], xs[8];
 #pragma unroll
     for (int q = 0; q < 8; q++) us[q] = j + q < k1 ? a.col[j + q] : -1;
@@ -268,8 +287,26 @@ __device__ void resolve_warp(const CfArgs& a, i32 v, u32* bm, int lane) {
   const i64 rs = a.rowptr[v];
   const i64 k0 = rs + __ldcg(rec), k1 = rs + __ldcg(rec + 1);
   const int nw = (int)__ldcg(rec + 2);
+  const u32 nopen = __ldcg(rec + 3);
   bm[lane] = lane < nw ? __ldcg(rec + CF_HDR + lane) : 0u;
   __syncwarp();
+  if (nopen != OPEN_WALK) {
+    // only the intra members that were open at the first pass can add colours
+    for (u32 k = lane; k < nopen; k += 32) {
+      const i32 u = (i32)__ldcg(rec + CF_HDR + nw + k);
+      const i32 x = wait_final(a, u);
+      const i32 c = -x - 2;
+      if (c >= 1 && c <= CF_WORDS * 32) atomicOr(bm + ((c - 1) >> 5), 1u << ((c - 1) & 31));
+    }
+    __syncwarp();
+    const i32 t = warp_mex(bm, lane);
+    if (lane == 0) {
+      if (t == 0) atomicOr(a.cnt + 2, 1u);
+      publish(a, v, t == 0 ? 1 : t);
+    }
+    __syncwarp();
+    return;
+  }
   for (i64 j = k0 + lane; j < k1; j += 32 * 8) {
     i32 us[8], xs[8];
 #pragma unroll
@@ -299,6 +336,9 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
   __shared__ u32 wbm[CF_WARPS][CF_WORDS];
   __shared__ u32 cbm[CF_WORDS];
   __shared__ int cred[3][CF_WARPS];
+  __shared__ i32 wlist[CF_WARPS][CF_OPEN];  // open intra members of a long row (first pass)
+  __shared__ i32 clist[CF_OPEN];
+  __shared__ int wlen[CF_WARPS], clen;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u32* bm = wbm[wid];
   const i64 gw = (i64)blockIdx.x * CF_WARPS + wid, nwarps = (i64)gridDim.x * CF_WARPS;
@@ -346,9 +386,10 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
       for (unsigned h = blockIdx.x; h < nc; h += gridDim.x) {
         const i32 vh = __ldcg(a.big[1] + h);
         if (threadIdx.x < CF_WORDS) cbm[threadIdx.x] = 0;
+        if (threadIdx.x == 0) clen = 0;
         __syncthreads();
         RowScan r;
-        first_scan(a, vh, s0, threadIdx.x, CF_THREADS, true, cbm, r);
+        first_scan(a, vh, s0, threadIdx.x, CF_THREADS, true, cbm, r, clist, &clen);
         r.intra = __reduce_add_sync(FULLM, r.intra);
         r.nlt0 = __reduce_add_sync(FULLM, r.nlt0);
         r.nltv = __reduce_add_sync(FULLM, r.nltv);
@@ -363,21 +404,23 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
           t.intra = __reduce_add_sync(FULLM, t.intra);
           t.nlt0 = __reduce_add_sync(FULLM, t.nlt0);
           t.nltv = __reduce_add_sync(FULLM, t.nltv);
-          first_finish(a, vh, t, cbm, lane);
+          first_finish(a, vh, t, cbm, lane, clist, clen);
         }
         __syncthreads();
       }
       for (i64 h = gw; h < nwr; h += nwarps) {
         const i32 vl = __ldcg(a.big[0] + h);
         bm[lane] = 0;
+        if (lane == 0) wlen[wid] = 0;
         __syncwarp();
         RowScan r;
-        first_scan(a, vl, s0, lane, 32, false, bm, r);
+        first_scan(a, vl, s0, lane, 32, false, bm, r, wlist[wid], &wlen[wid]);
         r.intra = __reduce_add_sync(FULLM, r.intra);
         r.nlt0 = __reduce_add_sync(FULLM, r.nlt0);
         r.nltv = __reduce_add_sync(FULLM, r.nltv);
         __syncwarp();
-        first_finish(a, vl, r, bm, lane);
+        __syncwarp();
+        first_finish(a, vl, r, bm, lane, wlist[wid], wlen[wid]);
         __syncwarp();
       }
     }
@@ -456,7 +499,8 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   i64 nnz = 0;
   CUDA_CHECK(cudaMemcpyAsync(&nnz, L.rowptr + nv, sizeof(i64), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
-  const i64 pool_words = nnz / 32 + (i64)(CF_HDR + 4) * nwl + 4096;
+  // bitmaps (<= deg/32 + 2 words), headers, and open lids (<= intra entries <= nnz)
+  const i64 pool_words = nnz / 32 + (i64)(CF_HDR + 4) * nwl + std::min<i64>(nnz, (i64)CF_OPEN * nwl) + 4096;
   S.pool.reserve(pool_words, s);
   S.pool_top.reserve(1, s);
   S.pool_top.zero(s);

@@ -111,6 +111,7 @@ void select_flagged_base(const uint8_t* flags, i64 n, i32 base, i32* out, i64* n
 void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* out, i64* n_out,
                            cudaStream_t s);
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s);
+i64 unique_u64(const u64* in, i64 n, u64* out, cudaStream_t s);  // sorted input; returns count
 void narrow_ids_checked(const i64* src, i64 k, i64 n, bool src_on_device, i32* out, cudaStream_t s,
                         const char* what);
 void sort_i32(i32* keys, i64 n, cudaStream_t s);  // ascending, in place (non-negative keys)
@@ -145,6 +146,7 @@ struct DetectScratch {
   DBuf<uint8_t> mark;
   DBuf<i64> narows;
   DBuf<i32> chl, chh;  // changed vertices, light / heavy rows (free-running D1)
+  DBuf<u64> keys, ukeys;  // keyed event emission (sequential D1)
   DBuf<unsigned long long> nch;
   bool prev_valid = false;
 };

@@ -230,6 +230,23 @@ void narrow_ids_checked(const i64* src, i64 k, i64 n, bool src_on_device, i32* o
   CHROMA_REQUIRE(hb == 0, CHROMA_EVALUE, what);
 }
 
+// distinct sorted keys of in[0..n) -> out; returns the count (one sync)
+i64 unique_u64(const u64* in, i64 n, u64* out, cudaStream_t s) {
+  if (n <= 0) return 0;
+  static thread_local DBuf<i64>* cnts[64] = {};
+  DBuf<i64>& c = per_device_scratch(cnts);
+  c.reserve(1, s);
+  size_t bytes = 0;
+  CUDA_CHECK(cub::DeviceSelect::Unique(nullptr, bytes, in, out, c.p, n, s));
+  t_cub_tmp.reserve((i64)bytes, s);
+  CUDA_CHECK(cub::DeviceSelect::Unique(t_cub_tmp.p, bytes, in, out, c.p, n, s));
+  count_launch();
+  i64 k = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&k, c.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  return k;
+}
+
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s) {
   if (n <= 0) return;
   size_t bytes = 0;
