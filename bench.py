@@ -379,6 +379,15 @@ def main():
         dist.all_gather(bufs, own)
         return torch.cat(bufs).cpu().numpy()  # partition_block: owned ranges are contiguous in gid order
 
+    # per-phase device times and the halo (RoundReport fields, chroma/runtime.py:83-108)
+    phases = {"color_ms": 1e3 * sum(r.time_color_s for r in reports),
+              "comm_ms": 1e3 * sum(r.time_comm_s for r in reports),
+              "detect_ms": 1e3 * sum(r.time_detect_s for r in reports)}
+    pairs = sum(r.bytes_sent for r in reports) // 12  # reference accounting: 12 B per (gid, colour)
+    halo = {"pairs_per_step": pairs, "bytes_sent_reference_accounting": 12 * pairs,
+            "payload_bytes": 4 * pairs,  # int32 colour per ghost copy on the wire
+            "nvlink_GBps": (4 * pairs / (phases["comm_ms"] * 1e-3) / 1e9) if N > 1 and phases["comm_ms"] > 0 else None,
+            "nvlink_peak_GBps": "770 per direction (measured peer copy, B200_PROFILING.md)"}
     gcol = gather_colors()
     ncol = nviol = sha = None
     gold = wl.golden(N)
@@ -410,6 +419,9 @@ def main():
             fn, _ = V.color_stats(fcol)
             ref_n = ((gold or {}).get("run") or {}).get("colors")
             free = {"value": m * args.steps / Tf, "ms_per_step": 1e3 * Tf / args.steps, "rounds": len(freps),
+                    "phases_ms_rank0": {"color_ms": 1e3 * sum(r.time_color_s for r in freps),
+                                        "comm_ms": 1e3 * sum(r.time_comm_s for r in freps),
+                                        "detect_ms": 1e3 * sum(r.time_detect_s for r in freps)},
                     "colors": fn, "oracle_deterministic_colors": ref_n,
                     "within_5pct": (fn <= 1.05 * ref_n) if ref_n else None,
                     "violations": V.count_violations(g, fcol, wl.vmode)}
@@ -475,7 +487,7 @@ def main():
                 "config": {"workload": f"{wl.desc}, partition_block P={N}, {wl.algorithm}",
                            "n": g.num_vertices, "m": m, "ghost_layers": wl.gl, "rounds": len(reports),
                            "colors": ncol, "violations": nviol, "colour_sha256": sha,
-                           "parallelism": f"vertex-range x{N}",
+                           "parallelism": f"vertex-range x{N}", "phases_ms_rank0": phases, "halo": halo,
                            "caching": "none: every step rebuilds the colouring state (no per-world schedule)"
                                       if wl.name == "c3" else "per-world round-0 schedule built in warm-up",
                            "l2": f"inputs larger than L2 (int32 col {4 * len(g.col_indices) / 1e6:.0f} MB)"},
