@@ -1,4 +1,4 @@
-"""Dev probe (round 2): D2 / PD2 free and deterministic timings (C4, C5)."""
+"""Probe: D2 / PD2 free and deterministic timings (C4, C5) at P = 1, 8 (virtual ranks)."""
 import hashlib, sys, os, time
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -1,7 +1,9 @@
-"""Dev probe (round 2): deterministic D1 on R-MAT at P=1 with the chunk trace."""
+"""Probe: deterministic D1 on R-MAT at P ranks (virtual), device times and colour sha.
+CHROMA_GS_CHUNK_TRACE=1 prints the chunked kernel's phase times per call."""
 import hashlib, sys, os
-import numpy as np, torch
+import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("CHROMA_MULTI_GPU", "0")
 from paper_2107_00075_b200 import graph as G, partition as PT, runtime as RT, protocol as R, _lib
 import ctypes as C
 scale = int(sys.argv[1]); P = int(sys.argv[2]) if len(sys.argv) > 2 else 1
