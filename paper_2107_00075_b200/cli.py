@@ -111,7 +111,7 @@ def _run_once(g, mask, args, ranks):
                    "recolor_degrees": args.recolor_degrees, "deterministic": args.deterministic,
                    "free": args.free, "eb_threshold": args.eb_threshold, "graph": args.graph or args.gen},
         "graph_stats": {"num_vertices": st.num_vertices, "num_edges": st.num_edges,
-                        "avg_degree": st.avg_degree, "delta_max": st.delta_max},
+                        "avg_degree": st.delta_avg, "delta_max": st.delta_max},
         "mode": mode.value, "ranks": ranks, "seed": args.seed,
         "rounds": [r.to_dict() for r in reports],
         "total_colors": int(len(np.unique(colors[colors > 0]))) if colors is not None else None,

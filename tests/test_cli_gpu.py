@@ -31,12 +31,12 @@ def test_color_d2_and_verify_roundtrip(tmp_path, capsys):
     cfile = tmp_path / "c.txt"
     assert cli.main(["color", "--gen", "gnp:100,0.1,7", "--mode", "d2", "--ranks", "2",
                      "--colors-out", str(cfile)]) == 0
-    gfile = tmp_path / "g.el"
+    gfile = tmp_path / "g.chrg"
     from paper_2107_00075_b200 import graph as G
     g = G.gen_random_gnp(100, 0.1, 7)
+    G.save_csr_cache(g, str(gfile))  # the CHRG v1 cache keeps n (an edge list would infer it)
     src = np.repeat(np.arange(g.num_vertices), np.diff(g.row_offsets))
     keep = src < g.col_indices
-    np.savetxt(gfile, np.column_stack([src[keep], g.col_indices[keep]]), fmt="%d")
     assert cli.main(["verify", "--graph", str(gfile), "--colors", str(cfile), "--mode", "d2"]) == 0
     bad = np.loadtxt(cfile, dtype=np.int64)
     u, w = int(src[keep][0]), int(g.col_indices[keep][0])
