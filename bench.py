@@ -267,7 +267,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (oracle generator, same CSR as the GPU arm)",
-            "config": {"workload": f"{wl.desc}, partition_block P={P}, deterministic (oracle)",
+            "config": {"workload": (f"{wl.desc}, partition_block P={P}, gauss-seidel" if not sample else
+                                    f"{wl.desc} (bounded sample), partition_block P={P}, gauss-seidel"),
                        "n": n, "m": m, "rounds": len(reps), "colors": int(len(np.unique(colors[colors > 0]))),
                        "colour_sha256": sha,
                        "golden_match": (gold or {}).get("run", {}).get("sha256") == sha if gold else None,
