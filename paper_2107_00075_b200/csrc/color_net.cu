@@ -17,11 +17,13 @@
 //           pending members of that colour are uncoloured and form the next worklist.
 // Later iterations (few vertices) rebuild only the nets around the pending vertices.
 // Colours above 256 fall back to the vertex-centric kernels (color_free.cu).
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "kernels.cuh"
 
 namespace chroma {
+namespace cg = cooperative_groups;
 namespace {
 
 constexpr int NW = 4;                  // u64 words per net mask: colours 1..256
@@ -61,11 +63,25 @@ __device__ __forceinline__ void build_mask(const NetArgs& a, i32 u, int lane) {
   if (lane < NW) a.mask[(i64)u * NW + lane] = m[lane];
 }
 
-// all nets (warp per net)
+// all nets, GL lanes per net (four nets per warp; rows of ~32 entries take four
+// column loads per lane and three shuffle rounds)
 __global__ void k_masks_all(NetArgs a, i64 nv) {
-  const int lane = threadIdx.x & 31;
-  const i64 w0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
-  for (i64 u = w0; u < nv; u += nw) build_mask(a, (i32)u, lane);
+  const int lane = threadIdx.x & 31, sub = lane % GL;
+  const i64 gi = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / GL, ng = ((i64)gridDim.x * blockDim.x) / GL;
+  for (i64 base = 0; base < nv; base += ng) {  // uniform trip count per warp
+    const i64 u = base + gi;
+    unsigned long long m[NW] = {0, 0, 0, 0};
+    if (u < nv) {
+      const i64 rs = a.rowptr[u], re = a.rowptr[u + 1];
+      for (i64 j = rs + sub; j < re; j += GL) set_bit(m, a.colors[__ldcs(a.col + j)]);
+      if (a.full && sub == 0) set_bit(m, a.colors[u]);
+    }
+#pragma unroll
+    for (int w = 0; w < NW; w++)
+#pragma unroll
+      for (int o = GL / 2; o >= 1; o >>= 1) m[w] |= __shfl_xor_sync(FULLM, m[w], o);
+    if (u < nv && sub < NW) a.mask[u * NW + sub] = m[sub];
+  }
 }
 
 // nets adjacent to the pending vertices (warp per pending vertex, its row's nets)
@@ -80,13 +96,13 @@ __global__ void k_masks_around(NetArgs a) {
   }
 }
 
-// pick: GL lanes per pending vertex
-__global__ void k_pick(NetArgs a) {
+// pick for worklist positions [lo, hi): GL lanes per pending vertex
+__device__ __forceinline__ void pick_range(const NetArgs& a, i64 lo, i64 hi) {
   const int lane = threadIdx.x & 31, sub = lane % GL;
   const i64 gi = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / GL, ng = ((i64)gridDim.x * blockDim.x) / GL;
-  for (i64 base = 0; base < a.nwl; base += ng) {  // uniform trip count: shuffles below use all lanes
+  for (i64 base = lo; base < hi; base += ng) {  // uniform trip count: shuffles below use all lanes
     const i64 i = base + gi;
-    const bool act = i < a.nwl;
+    const bool act = i < hi;
     const i32 v = act ? a.wl[i] : 0;
     unsigned long long m[NW] = {0, 0, 0, 0};
     i64 rs = 0, re = 0;
@@ -125,8 +141,43 @@ __global__ void k_pick(NetArgs a) {
   }
 }
 
+__global__ void k_pick(NetArgs a) { pick_range(a, 0, a.nwl); }
+
+// the first pass's waves in one cooperative launch, a grid barrier between waves (a
+// wave's picks and mask updates are visible to the next one)
+__global__ void k_pick_waves(NetArgs a, int waves) {
+  cg::grid_group grid = cg::this_grid();
+  for (int w = 0; w < waves; w++) {
+    pick_range(a, a.nwl * w / waves, a.nwl * (w + 1) / waves);
+    grid.sync();
+  }
+}
+
+__device__ __forceinline__ void lose(const NetArgs& a, i32 x) {
+  if (atomicExch(a.colors + x, 0) != 0) {
+    const unsigned long long k = atomicAdd(a.nnext, 1ull);
+    a.next[k] = x;
+  }
+}
+
 // detect on one net u by one warp: the largest pending id per colour survives
 __device__ __forceinline__ void detect_net(const NetArgs& a, i32 u, int lane, i32* mx) {
+  const i64 rs0 = a.rowptr[u], re0 = a.rowptr[u + 1];
+  const i64 members = re0 - rs0 + (a.full ? 1 : 0);
+  if (members <= 32) {  // one member per lane: equal-colour groups by __match_any_sync
+    i32 x = -1, key = -1 - lane;
+    if (lane < members) {
+      x = lane < re0 - rs0 ? a.col[rs0 + lane] : u;
+      if (a.pend[x]) {
+        const i32 c = a.colors[x];
+        if (c >= 1) key = c;
+      }
+    }
+    const unsigned grp = __match_any_sync(FULLM, key);
+    const i32 top = __reduce_max_sync(grp, (unsigned)(x + 1)) - 1;  // x >= 0 inside a real group
+    if (key > 0 && x < top) lose(a, x);
+    return;
+  }
   for (int k = lane; k < NCOL + 2; k += 32) mx[k] = -1;
   __syncwarp();
   const i64 rs = a.rowptr[u], re = a.rowptr[u + 1];
@@ -144,12 +195,7 @@ __device__ __forceinline__ void detect_net(const NetArgs& a, i32 u, int lane, i3
     const i32 x = j < re ? a.col[j] : u;
     if (!a.pend[x]) continue;
     const i32 c = a.colors[x];
-    if (c >= 1 && c <= NCOL + 1 && mx[c] > x && a.colors[x] != 0) {
-      if (atomicExch(a.colors + x, 0) != 0) {
-        const unsigned long long k = atomicAdd(a.nnext, 1ull);
-        a.next[k] = x;
-      }
-    }
+    if (c >= 1 && c <= NCOL + 1 && mx[c] > x && a.colors[x] != 0) lose(a, x);
   }
   __syncwarp();
 }
@@ -243,14 +289,19 @@ bool launch_free_net(const i64* rowptr, const i32* col, i64 nv, i32* colors, con
     // colours of the earlier ones in the masks, so fewer equal picks collide (the
     // colour count stays near sequential first fit's)
     const int waves = it == 0 ? (int)std::min<i64>(net_waves(), std::max<i64>(1, n / 1024)) : 1;
-    for (int wv = 0; wv < waves; wv++) {
-      NetArgs b = a;
-      const i64 lo = n * wv / waves, hi = n * (wv + 1) / waves;
-      b.wl = a.wl + lo;
-      b.nwl = hi - lo;
-      k_pick<<<G(b.nwl * GL), 256, 0, s>>>(b);
+    if (waves > 1) {
+      static int blocks[64] = {};  // co-resident blocks per SM, per device
+      int dev = 0;
+      CUDA_CHECK(cudaGetDevice(&dev));
+      int& bps = blocks[dev & 63];
+      if (!bps) CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_pick_waves, 256, 0));
+      const int grid = std::min<i64>(std::max(1, bps) * num_sms(), std::max<i64>(1, (n / waves + 1) * GL / 256 + 1));
+      int wv = waves;
+      void* args[] = {&a, &wv};
+      CUDA_CHECK(cudaLaunchCooperativeKernel((void*)k_pick_waves, grid, 256, args, 0, s));
+    } else {
+      k_pick<<<G(n * GL), 256, 0, s>>>(a);
     }
-    count_launch(waves - 1);
     if (all) k_detect_all<<<num_sms() * 16, 256, 0, s>>>(a, nv);
     else k_detect_around<<<G(n * 32), 256, 0, s>>>(a);
     k_set_pend<<<G(n), 256, 0, s>>>(a.wl, n, a.pend, 0);
