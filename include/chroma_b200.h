@@ -45,6 +45,7 @@ extern "C" {
 #define CHROMA_ALGO_GAUSS_SEIDEL 0   /* deterministic=True: ascending-lid first fit, bit-exact */
 #define CHROMA_ALGO_FREE 1           /* deterministic=False: free-running speculative (B200)   */
 #define CHROMA_ALGO_JACOBI 2         /* deterministic=False, jacobi_exact: reference sweeps   */
+#define CHROMA_ALGO_JACOBI_EB 3      /* same sweeps, Kernel.EDGE_BASED (chroma/localcolor.py:181-195) */
 
 typedef struct chroma_csr chroma_csr;      /* a device-resident CSR graph        */
 typedef struct chroma_world chroma_world;  /* device-resident ranks + routing    */

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libchroma_b200.so")
 OK, EVALUE, EPROTOCOL, ENONCONV, ERUNTIME, ECUDA = range(6)
 DEVICE_PTRS = 1
 MODE = {"d1": 0, "d1-2gl": 1, "d2": 2, "pd2": 3}
-ALGO_GS, ALGO_FREE, ALGO_JACOBI = 0, 1, 2
+ALGO_GS, ALGO_FREE, ALGO_JACOBI, ALGO_JACOBI_EB = 0, 1, 2, 3
 
 
 class RoundReportC(C.Structure):

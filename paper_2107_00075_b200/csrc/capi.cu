@@ -579,7 +579,7 @@ int chroma_run_distributed(chroma_world* h, int mode, int rd, int algo, int max_
   int st = CHROMA_OK;
   const int g = guarded([&] {
     CHROMA_REQUIRE(mode >= 0 && mode <= 3, CHROMA_EVALUE, "unknown mode");
-    CHROMA_REQUIRE(algo >= 0 && algo <= 2, CHROMA_EVALUE, "unknown algorithm");
+    CHROMA_REQUIRE(algo >= 0 && algo <= 3, CHROMA_EVALUE, "unknown algorithm");
     st = run_distributed(*h->w, mode, rd != 0, algo, max_rounds, colors_out, reports, recolored, cap, n_reports,
                          dev(flags));
     if (st == CHROMA_ENONCONV) set_last_error("no convergence after " + std::to_string(max_rounds) + " rounds");

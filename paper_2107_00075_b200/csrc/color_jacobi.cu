@@ -85,9 +85,122 @@ __global__ void k_losers(const i64* rowptr, const i32* col, const i32* colors, c
   }
 }
 
+// ---------------------------------------------------------------- edge-based (EB)
+// chroma/localcolor.py:181-195 (Kernel.EDGE_BASED, chosen when delta_max exceeds the
+// threshold, 55-61): the same proposals and losers (F3), computed edge-parallel so a
+// hub row is spread over many threads.  The pending rows' entries are flattened by an
+// exclusive scan of their lengths (eoff); each thread takes EB_CHUNK consecutive
+// entries, finds its first row by binary search and walks on (merge path).
+constexpr int EB_CHUNK = 16;
+
+__global__ void k_eb_lengths(const i64* rowptr, const i32* pending, i64 np, i64* len) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < np; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = pending[i];
+    len[i] = rowptr[v + 1] - rowptr[v];
+  }
+}
+
+__device__ __forceinline__ i64 eb_row_of(const i64* eoff, i64 np, i64 e) {
+  i64 lo = 0, hi = np;  // last i with eoff[i] <= e
+  while (hi - lo > 1) {
+    const i64 mid = (lo + hi) >> 1;
+    if (eoff[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// OR the colours of window [base, base + WIN) into the per-row masks of unresolved rows
+__global__ void k_eb_masks(const i64* rowptr, const i32* col, const i32* colors, const i32* pending, i64 np,
+                           const i64* eoff, i64 E, i32 base, const i32* prop, u32* mask) {
+  for (i64 c0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) * EB_CHUNK; c0 < E;
+       c0 += (i64)gridDim.x * blockDim.x * EB_CHUNK) {
+    i64 i = eb_row_of(eoff, np, c0);
+    const i64 c1 = c0 + EB_CHUNK < E ? c0 + EB_CHUNK : E;
+    for (i64 e = c0; e < c1; e++) {
+      while (i + 1 < np && eoff[i + 1] <= e) i++;
+      if (prop[i] != 0) continue;  // resolved in an earlier window
+      const i32 v = pending[i];
+      const i32 x = col[rowptr[v] + (e - eoff[i])];
+      const i32 o = colors[x] - base;
+      if (o >= 0 && o < WIN) atomicOr(mask + i * WORDS + (o >> 5), 1u << (o & 31));
+    }
+  }
+}
+
+// first free colour of the window per unresolved row; *left counts rows still full
+__global__ void k_eb_pick(i64 np, i32 base, const u32* mask, i32* prop, unsigned long long* left) {
+  unsigned long long full = 0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < np; i += (i64)gridDim.x * blockDim.x) {
+    if (prop[i] != 0) continue;
+    int r = 0;
+#pragma unroll
+    for (int w = 0; w < WORDS; w++) {
+      const u32 mw = mask[i * WORDS + w];
+      if (!r && mw != FULL) r = w * 32 + __ffs(~mw);
+    }
+    if (r) prop[i] = base + r - 1;
+    else full++;
+  }
+  if (full) atomicAdd(left, full);
+}
+
+// v loses iff an equal-coloured neighbour has a larger id or is outside the round
+__global__ void k_eb_losers(const i64* rowptr, const i32* col, const i32* colors, const i32* pending, i64 np,
+                            const i64* eoff, i64 E, const uint8_t* in_round, uint8_t* lose) {
+  for (i64 c0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) * EB_CHUNK; c0 < E;
+       c0 += (i64)gridDim.x * blockDim.x * EB_CHUNK) {
+    i64 i = eb_row_of(eoff, np, c0);
+    const i64 c1 = c0 + EB_CHUNK < E ? c0 + EB_CHUNK : E;
+    for (i64 e = c0; e < c1; e++) {
+      while (i + 1 < np && eoff[i + 1] <= e) i++;
+      const i32 v = pending[i];
+      const i32 x = col[rowptr[v] + (e - eoff[i])];
+      if (colors[x] == colors[v] && (x > v || !in_round[x])) lose[i] = 1;
+    }
+  }
+}
+
 }  // namespace
 
 static int warp_grid(i64 n) { return grid_for(n * 32, 256, num_sms() * 16); }
+
+// Edge-based Jacobi sweep pieces (distance 1): proposals into prop, then (after the
+// caller's commit) losers into lose.  np: exact pending count.
+void launch_jacobi_eb(const i64* rowptr, const i32* col, i32* colors, const i32* pending, i64 np, i32* prop,
+                      const uint8_t* in_round, uint8_t* lose, EbScratch& S, cudaStream_t s) {
+  if (np <= 0) return;
+  S.len.reserve(np + 1, s);
+  S.eoff.reserve(np + 1, s);
+  k_eb_lengths<<<grid_for(np, 256, num_sms() * 16), 256, 0, s>>>(rowptr, pending, np, S.len.p);
+  CUDA_CHECK(cudaMemsetAsync(S.len.p + np, 0, sizeof(i64), s));
+  exclusive_scan_i64(S.len.p, S.eoff.p, np + 1, s);
+  i64 E = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&E, S.eoff.p + np, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  S.mask.reserve(np * WORDS, s);
+  S.left.reserve(1, s);
+  CUDA_CHECK(cudaMemsetAsync(prop, 0, sizeof(i32) * np, s));
+  const int ge = grid_for(std::max<i64>((E + EB_CHUNK - 1) / EB_CHUNK, 1), 256, num_sms() * 16);
+  for (i32 base = 1;; base += WIN) {
+    CUDA_CHECK(cudaMemsetAsync(S.mask.p, 0, sizeof(u32) * WORDS * np, s));
+    CUDA_CHECK(cudaMemsetAsync(S.left.p, 0, sizeof(unsigned long long), s));
+    if (E > 0) k_eb_masks<<<ge, 256, 0, s>>>(rowptr, col, colors, pending, np, S.eoff.p, E, base, prop, S.mask.p);
+    k_eb_pick<<<grid_for(np, 256, num_sms() * 16), 256, 0, s>>>(np, base, S.mask.p, prop, S.left.p);
+    count_launch(2);
+    unsigned long long left = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&left, S.left.p, sizeof(left), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (!left) break;
+  }
+  // commit the proposals (chroma/localcolor.py:222), then the edge-parallel loser scan
+  S.np.reserve(1, s);
+  CUDA_CHECK(cudaMemcpyAsync(S.np.p, &np, sizeof(i64), cudaMemcpyHostToDevice, s));
+  launch_scatter_idx_values(colors, pending, prop, S.np.p, np, s);
+  CUDA_CHECK(cudaMemsetAsync(lose, 0, np, s));
+  if (E > 0) k_eb_losers<<<ge, 256, 0, s>>>(rowptr, col, colors, pending, np, S.eoff.p, E, in_round, lose);
+  count_launch(2);
+  CUDA_CHECK(cudaGetLastError());
+}
 
 void launch_jacobi_propose(const i64* rowptr, const i32* col, const i32* colors, const i32* pending,
                            const i64* np_dev, i64 np_max, i32* prop, int dist, bool partial,

@@ -49,6 +49,16 @@ void launch_jacobi_losers(const i64* rowptr, const i32* col, i32* colors, const 
                           const i64* np_dev, i64 np_max, const i32* prop, const uint8_t* in_round,
                           uint8_t* lose, int dist, bool partial, cudaStream_t s);
 
+// Edge-based Jacobi sweep (Kernel.EDGE_BASED, distance 1): proposals into prop, the
+// commit, and losers into lose, edge-parallel over the pending rows.
+struct EbScratch {
+  DBuf<i64> len, eoff, np;
+  DBuf<u32> mask;
+  DBuf<unsigned long long> left;
+};
+void launch_jacobi_eb(const i64* rowptr, const i32* col, i32* colors, const i32* pending, i64 np, i32* prop,
+                      const uint8_t* in_round, uint8_t* lose, EbScratch& S, cudaStream_t s);
+
 // Free-running speculative colouring (deterministic=False, algorithm="free").
 // Pending vertices are kept in light (warp per vertex), heavy (CTA per vertex) and
 // tiny (8 lanes per vertex) lists, double-buffered by parity p; cnt[3p + {0,1,2}]

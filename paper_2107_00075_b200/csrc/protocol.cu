@@ -298,7 +298,9 @@ gauss_seidel:
     if (!colors_nonneg) launch_scatter_from(colors, S.val.p, wl, nwl, nwl_max, s);
     return;
   }
-  // Jacobi sweeps (chroma/localcolor.py:214-227, 292-303)
+  // Jacobi sweeps (chroma/localcolor.py:214-227, 292-303); CHROMA_ALGO_JACOBI_EB takes
+  // the edge-based kernels (chroma/localcolor.py:181-195) -- same losers (F3)
+  const bool edge_based = algo == CHROMA_ALGO_JACOBI_EB;
   S.in_round.reserve(nv, s);
   CUDA_CHECK(cudaMemsetAsync(S.in_round.p, 0, nv, s));
   k_set_u8_idx<<<G(nwl_max), 256, 0, s>>>(S.in_round.p, wl, nwl, 1);
@@ -314,9 +316,13 @@ gauss_seidel:
   i64 np = read_i64(nwl, s);  // exact count: the compaction below takes a host length
   for (int sweep = 0; sweep < MAX_SWEEPS; sweep++) {
     if (np == 0) return;
-    launch_jacobi_propose(rowptr, col, colors, pend, S.np2.p, np, S.prop.p, dist, partial, s);
-    launch_jacobi_losers(rowptr, col, colors, pend, S.np2.p, np, S.prop.p, S.in_round.p, S.flags.p,
-                         dist, partial, s);
+    if (edge_based && dist == 1) {
+      launch_jacobi_eb(rowptr, col, colors, pend, np, S.prop.p, S.in_round.p, S.flags.p, S.eb, s);
+    } else {
+      launch_jacobi_propose(rowptr, col, colors, pend, S.np2.p, np, S.prop.p, dist, partial, s);
+      launch_jacobi_losers(rowptr, col, colors, pend, S.np2.p, np, S.prop.p, S.in_round.p, S.flags.p,
+                           dist, partial, s);
+    }
     select_flagged_values(pend, S.flags.p, np, S.pend2.p, S.np2.p, s);
     np = read_i64(S.np2.p, s);
     launch_scatter_const(colors, S.pend2.p, S.np2.p, np, 0, s);
@@ -458,6 +464,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   // ordered kernel on hub-free worklists -- levels are built for bounded-degree graphs.
   static const i64 level_max_deg = env_i64("CHROMA_LEVEL_MAX_DEG", 1024);
   const bool fast = algo == CHROMA_ALGO_FREE && !no_fast && (!w.connected || w.p2p || w.P == 1);
+  const bool is_jacobi = algo == CHROMA_ALGO_JACOBI || algo == CHROMA_ALGO_JACOBI_EB;
   // free-running D1 over several ranks: colour the hubs of all ranks first (hubs.cu)
   static const bool no_hubs = std::getenv("CHROMA_NO_HUBS") != nullptr;
   const i64 hub_deg = env_i64("CHROMA_HUB_DEG", 4096);  // read per call (tests vary it)
@@ -537,7 +544,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
       // worklist (ordered compaction: ascending local id)
       // Jacobi re-colours uncoloured ghosts too (F7); the other modes only owned ones
       k_flag_worklist<<<G(w.NL), 256, 0, s>>>(w.colors.p, w.owned_flag.p, w.NL,
-                                              round == 0 || algo != CHROMA_ALGO_JACOBI, w.cs.flags.p);
+                                              round == 0 || !is_jacobi, w.cs.flags.p);
       count_launch();
       select_flagged(w.cs.flags.p, w.NL, w.cs.wl.p, w.cs.nwl.p, s);
       nwl_host = w.NL;
@@ -545,7 +552,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     k_count_recolored<<<std::min(G(w.NL), num_sms() * 2), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
                                               w.rank_hi - w.rank_lo, w.stats.p);
     count_launch();
-    const bool gs_like = algo != CHROMA_ALGO_JACOBI;
+    const bool gs_like = !is_jacobi;
     // round 0 colours every owned vertex: claim them by DAG level (cached per world)
     w.cs.level_wl = nullptr;
     // The schedule is built from round 0's full owned worklist and cached per world:

@@ -59,6 +59,7 @@ struct ColorScratch {
   FreeWaveScratch fw;
   ChunkedScratch chunked;
   NetScratch net;
+  EbScratch eb;
   bool upper_zero = false;  // gs_chunked: no neighbour above a member is coloured yet
 };
 

@@ -8,9 +8,9 @@
                          larger-id-wins loser rule (chroma/localcolor.py:214-227,
                          292-303), also bit-exact.  ``set_free_running(True)`` switches
                          to the B200 free-running speculative kernel instead.
-The VB / EB kernel choice selects the same losers in the reference (F3); on the GPU
-the edge-parallel flattening inside the colouring kernel load-balances any degree
-distribution, so the choice is accepted and recorded but does not change results.
+The VB / EB kernel choice selects the same losers in the reference (F3); on the GPU the
+Jacobi sweep runs warp-per-vertex kernels for VB and edge-parallel (merge-path over the
+pending rows' entries) kernels for EB -- same colours, different load balance.
 """
 from __future__ import annotations
 
@@ -145,7 +145,7 @@ def _world_of(lg):
     return wh if isinstance(getattr(lg, "rank", None), int) and wh is not None else None
 
 
-def _color(lg, colors, worklist, dist: int, partial: bool, deterministic: bool):
+def _color(lg, colors, worklist, dist: int, partial: bool, deterministic: bool, edge_based: bool = False):
     wl = _lib.i64(worklist).ravel()
     if wl.size == 0:
         return colors
@@ -155,6 +155,8 @@ def _color(lg, colors, worklist, dist: int, partial: bool, deterministic: bool):
     buf = np.ascontiguousarray(colors, dtype=np.int32)
     wh = _world_of(lg)
     algo = _algo(deterministic)
+    if algo == _lib.ALGO_JACOBI and edge_based and dist == 1:
+        algo = _lib.ALGO_JACOBI_EB
     if wh is not None:
         _lib.check(_lib.lib().chroma_world_color(wh.h, lg.rank, _lib.ptr(buf), _lib.ptr(wl), wl.size,
                                                  dist, int(partial), algo), "speculative_color")
@@ -169,8 +171,10 @@ def _color(lg, colors, worklist, dist: int, partial: bool, deterministic: bool):
 
 def speculative_color(lg, colors, worklist, kernel: KernelChoice | None = None,
                       deterministic: bool = False) -> np.ndarray:
-    """Distance-1 colouring of `worklist` in place (chroma/localcolor.py:198-227)."""
-    return _color(lg, colors, worklist, 1, False, deterministic)
+    """Distance-1 colouring of `worklist` in place (chroma/localcolor.py:198-227).
+    kernel.kind EDGE_BASED runs the edge-parallel Jacobi kernels (181-195)."""
+    eb = kernel is not None and kernel.kind is Kernel.EDGE_BASED
+    return _color(lg, colors, worklist, 1, False, deterministic, eb)
 
 
 def speculative_color_d2(lg, colors, worklist, partial: bool = False,

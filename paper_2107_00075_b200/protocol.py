@@ -17,7 +17,7 @@ from enum import Enum
 import numpy as np
 
 from . import _lib
-from .localcolor import KernelChoice, select_kernel, _algo
+from .localcolor import Kernel, KernelChoice, select_kernel, _algo
 from .runtime import LocalGraph, RankWorld, RoundReport
 
 __all__ = ["Mode", "AlgorithmConfig", "NonConvergenceError", "gid_rand", "gid_rand_array",
@@ -189,7 +189,12 @@ def run_distributed(world, cfg: AlgorithmConfig, out=None):
         raise ValueError(f"mode {mode.value} needs {needed} ghost layer(s), "
                          f"world was built with {world.ghost_layers}")
     world.reset_exchange_state()
-    select_kernel(world.source_stats, cfg.kernel)
+    # Kernel.EDGE_BASED iff delta_max > threshold (chroma/protocol.py:281): the Jacobi
+    # sweeps then run edge-parallel (same losers, F3)
+    kernel = select_kernel(world.source_stats, cfg.kernel)
+    algo = cfg.algo_code()
+    if algo == _lib.ALGO_JACOBI and kernel.kind is Kernel.EDGE_BASED and mode in (Mode.D1, Mode.D1_2GL):
+        algo = _lib.ALGO_JACOBI_EB
     P = world.num_ranks
     cap = cfg.max_rounds + 2
     rep = (_lib.RoundReportC * cap)()
@@ -197,7 +202,7 @@ def run_distributed(world, cfg: AlgorithmConfig, out=None):
     nrep = C.c_int64(0)
     n_out = world.output_length() if hasattr(world, "output_length") else world.num_global_vertices
     if hasattr(world, "run") and hasattr(world, "devices"):  # MultiDeviceWorld
-        colors, st, rep, rec, nr = world.run(_lib.MODE[mode.value], bool(cfg.recolor_degrees), cfg.algo_code(),
+        colors, st, rep, rec, nr = world.run(_lib.MODE[mode.value], bool(cfg.recolor_degrees), algo,
                                              int(cfg.max_rounds))
         reports = _reports_from(rep, rec, nr, P)
         world.total_bytes = sum(r.bytes_sent for r in reports)
@@ -219,7 +224,7 @@ def run_distributed(world, cfg: AlgorithmConfig, out=None):
         colors = _host_colors(n_out)
         optr, flags = _lib.ptr(colors), 0
     st = _lib.lib().chroma_run_distributed(world.handle.h, _lib.MODE[mode.value],
-                                           int(bool(cfg.recolor_degrees)), cfg.algo_code(),
+                                           int(bool(cfg.recolor_degrees)), algo,
                                            int(cfg.max_rounds), optr, rep, _lib.ptr(rec),
                                            cap, C.byref(nrep), flags)
     reports = _reports_from(rep, rec, nrep.value, P)
