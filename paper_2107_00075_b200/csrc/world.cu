@@ -561,6 +561,27 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
     for (i32 r = lo; r < hi; r++) {
       RankTmp& T = tmps[(size_t)(r - lo)];
       T.m.rank = r;
+      if (P == 1) {
+        // one rank owns every vertex: no ghosts, the local graph is the graph itself
+        // (lid = gid), boundary sets are empty, every edge is local
+        T.lgids.alloc(std::max<i64>(n, 1), s);
+        launch_iota_i32(T.lgids.p, n, 0, s);
+        T.m.owned = n; T.m.ghost = 0; T.m.l1 = 0;
+        T.m.nnz = nnz;
+        T.lrow = std::move(goff);
+        T.lcol = std::move(gcol);
+        T.b1.alloc(1, s);
+        T.b2.alloc(1, s);
+        T.m.nb1 = T.m.nb2 = 0;
+        T.m.e_local = nnz / 2;
+        T.m.e_ghost = 0;
+        T.gids.alloc(n + 1, s);
+        T.deg.alloc(n + 1, s);
+        T.ghost_owner.alloc(1, s);
+        k_local_meta<<<G(n), 256, 0, s>>>(T.lgids.p, n, n, T.lrow.p, owner.p, T.gids.p, T.deg.p, T.ghost_owner.p);
+        count_launch();
+        continue;
+      }
       T.lgids.alloc(std::max<i64>(n, 1), s);
       // owned (ascending gid)
       k_flag_eq_i32<<<G(n), 256, 0, s>>>(owner.p, n, r, flag.p);
@@ -653,8 +674,15 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
     CHROMA_REQUIRE(NL < INT32_MAX, CHROMA_EVALUE, "local vertex count exceeds int32");
     w->NL = NL; w->NNZ = NNZ; w->NGHOST = NG; w->NB1 = NB1; w->NB2 = NB2;
     w->g.device = device; w->g.stream = s; w->g.n = NL; w->g.nnz = NNZ;
-    w->g.rowptr.alloc(NL + 1, s);
-    w->g.col.alloc(std::max<i64>(NNZ, 1), s);
+    // a single rank at offset 0 hands its CSR over instead of copying it
+    const bool take = tmps.size() == 1 && tmps[0].m.lid_off == 0 && tmps[0].m.nnz_off == 0;
+    if (take) {
+      w->g.rowptr = std::move(tmps[0].lrow);
+      w->g.col = std::move(tmps[0].lcol);
+    } else {
+      w->g.rowptr.alloc(NL + 1, s);
+      w->g.col.alloc(std::max<i64>(NNZ, 1), s);
+    }
     w->gids.alloc(NL + 1, s);
     w->deg.alloc(NL + 1, s);
     w->colors.alloc(NL + 1, s);
@@ -669,8 +697,10 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
     for (auto& T : tmps) {
       const RankMeta& m = T.m;
       const i64 nl = m.owned + m.ghost;
-      k_shift_i64<<<G(nl), 256, 0, s>>>(T.lrow.p, w->g.rowptr.p + m.lid_off, nl, m.nnz_off);
-      k_shift_i32<<<G(m.nnz), 256, 0, s>>>(T.lcol.p, w->g.col.p + m.nnz_off, m.nnz, (i32)m.lid_off);
+      if (!take) {
+        k_shift_i64<<<G(nl), 256, 0, s>>>(T.lrow.p, w->g.rowptr.p + m.lid_off, nl, m.nnz_off);
+        k_shift_i32<<<G(m.nnz), 256, 0, s>>>(T.lcol.p, w->g.col.p + m.nnz_off, m.nnz, (i32)m.lid_off);
+      }
       CUDA_CHECK(cudaMemcpyAsync(w->gids.p + m.lid_off, T.gids.p, sizeof(i64) * nl, cudaMemcpyDeviceToDevice, s));
       CUDA_CHECK(cudaMemcpyAsync(w->deg.p + m.lid_off, T.deg.p, sizeof(i32) * nl, cudaMemcpyDeviceToDevice, s));
       if (m.ghost)
@@ -684,7 +714,7 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
       count_launch(8);
       w->ranks.push_back(m);
     }
-    CUDA_CHECK(cudaMemcpyAsync(w->g.rowptr.p + NL, &NNZ, sizeof(i64), cudaMemcpyHostToDevice, s));
+    if (!take) CUDA_CHECK(cudaMemcpyAsync(w->g.rowptr.p + NL, &NNZ, sizeof(i64), cudaMemcpyHostToDevice, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
     tmps.clear();
 
