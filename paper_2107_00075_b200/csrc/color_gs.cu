@@ -415,8 +415,7 @@ gs_kernel(GsArgs a) {
 
 void launch_gs(const GsLaunch& L, cudaStream_t s) {
   // distance 1 in id order: the pre-scan-free kernel (color_gs_d1.cu)
-  static const bool generic = std::getenv("CHROMA_GS_GENERIC") != nullptr;
-  if ((!generic || L.level_mode) && launch_gs_d1(L, s)) return;
+  if (launch_gs_d1(L, s)) return;
   CHROMA_REQUIRE(!L.level_mode, CHROMA_ERUNTIME, "level schedules are distance-1 only");
   GsArgs a;
   a.rowptr = L.rowptr;

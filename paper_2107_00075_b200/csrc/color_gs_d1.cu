@@ -342,8 +342,7 @@ bool launch_gs_d1(const GsLaunch& L, cudaStream_t s) {
   a.nwl = L.nwl_dev;
   a.ticket = L.ticket;
   a.level_mode = L.level_mode;
-  static const int poll_env = std::getenv("CHROMA_GS_POLL_ALL") ? std::atoi(std::getenv("CHROMA_GS_POLL_ALL")) : -1;
-  a.poll_all = poll_env >= 0 ? poll_env != 0 : L.level_mode;
+  a.poll_all = L.level_mode;
   CUDA_CHECK(cudaMemsetAsync(L.ticket, 0, sizeof(unsigned long long), s));
   const i64 nchunks = (L.nwl_max + 31) / 32;
   static const int bps_env = std::getenv("CHROMA_GS_BPS") ? std::atoi(std::getenv("CHROMA_GS_BPS")) : 0;

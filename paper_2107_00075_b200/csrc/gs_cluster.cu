@@ -183,23 +183,10 @@ __global__ void k_ent_item(const i32* item_a, const i32* item_n, i64 nitems, i32
     for (i64 t = threadIdx.x; t < item_n[it]; t += blockDim.x) ent_item[item_a[it] + t] = (i32)it;
 }
 
-__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(a), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(g) : "memory");
-}
 __device__ __forceinline__ u32 shl1(u32 c) {
   u32 r;
   asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(c));
   return r;
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 struct ClusterArgs {
@@ -214,8 +201,6 @@ struct ClusterArgs {
   Own own;
   i32* val;
   const i32* old;
-  int exp;                  // dev experiments (timing only): 1 no remote loads, 2 no global store, 4 item_n from smem
-  unsigned long long* dbg;  // optional [8] clocks of CTA 0 (wait, colour, cluster sync, items, start, loop, end, issue)
 };
 
 template <int DW>
@@ -227,7 +212,6 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
   const int t = threadIdx.x;
   const i64 per_pad = (a.per + 15) / 16 * 16;
   unsigned char* col8 = smem;
-  const long long t_start = clock64();
   const i64 stage_bytes = ((i64)a.CAP * (a.DW + 1) + 4) * 4;  // one item: header, ids, slots
   unsigned char* stages = smem + per_pad + 16;
   const u32 mbar = (u32)__cvta_generic_to_shared(stages + (i64)S * stage_bytes);  // S mbarriers
@@ -291,9 +275,6 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     nx_sz = a.item_sz[k_begin + S - 1];
   }
   cluster.sync();
-  long long tw = 0, tc = 0, ts = 0, ni = 0, ti = 0;
-  const long long t_loop = clock64();
-  const bool dbg = a.dbg && r == 0 && t == 0;
   // Level barriers, split and item-driven.  Every CTA passes L barriers (one per
   // level), in order; it arrives at level l's barrier once its stores of level l are
   // done and waits only right before its first gathers of a later level, so stage
@@ -308,9 +289,7 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
   i64 cur = 0;           // barriers arrived at
   auto wait_level = [&]() {
     if (waiting) {
-      const long long c2 = dbg ? clock64() : 0;
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-      if (dbg) ts += clock64() - c2;
       waiting = false;
     }
   };
@@ -323,7 +302,6 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     }
   };
   for (i32 k = k_begin; k < k_end; k++) {
-    const long long c0 = dbg ? clock64() : 0;
     {
       const int q = (k - k_begin) % S;
       const u32 par = (u32)((k - k_begin) / S) & 1u;
@@ -336,8 +314,6 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
           : "memory");
     }
     __syncthreads();  // stage k landed; every thread is past item k - 1
-    const long long c1 = dbg ? clock64() : 0;
-    if (dbg) tw += c1 - c0, ni++;
     const unsigned char* st = stages + (i64)((k - k_begin) % S) * stage_bytes;
     const i32* sh = reinterpret_cast<const i32*>(st);
     const i32 n = sh[0];
@@ -423,8 +399,6 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
     }
     const u32 fb = f >> 16;
     if (act) col8[a.own.offset(v)] = (unsigned char)fb;
-    if (dbg) tc += clock64() - c1;
-    const long long c3 = dbg ? clock64() : 0;
     if (t == 0) {
       issue(k + S - 1, nx_o, nx_sz);  // into item k - 1's stage (all threads are past it)
       if (k + S < k_end) {
@@ -432,9 +406,7 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
         nx_sz = a.item_sz[k + S];
       }
     }
-    if (dbg) ti += clock64() - c3;
   }
-  const long long t_end = clock64();
   close_levels_below(a.L);
   wait_level();
   // colours back to global memory once, at the end (no global stores inside the
@@ -455,16 +427,6 @@ __global__ void __launch_bounds__(1024, 1) k_gs_cluster(ClusterArgs a) {
       for (int i = 0; i < 4; i++)
         if (x + i < a.nv && a.val[x + i] == PENDING) a.val[x + i] = (i32)((w4 >> (8 * i)) & 0xffu);
     }
-  }
-  if (dbg) {
-    a.dbg[0] = tw;
-    a.dbg[1] = tc;
-    a.dbg[2] = ts;
-    a.dbg[3] = ni;
-    a.dbg[4] = t_loop - t_start;
-    a.dbg[5] = t_end - t_loop;
-    a.dbg[6] = clock64() - t_end;
-    a.dbg[7] = ti;
   }
 }
 
@@ -537,9 +499,7 @@ bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, 
   i64 per = 0;
   const int logB = 10;
   const i64 nblocks = (nv + (1ll << logB) - 1) >> logB;
-  static const int cl_env = std::getenv("CHROMA_CLUSTER_SIZE") ? std::atoi(std::getenv("CHROMA_CLUSTER_SIZE")) : 0;
   for (int cl : {16, 8}) {
-    if (cl_env && cl != cl_env) continue;
     per = (nblocks + cl - 1) / cl << logB;  // colour bytes per CTA (whole blocks)
     const i64 per_pad = (per + 15) / 16 * 16;
     const i64 room = (i64)max_smem - per_pad - 16 - 1024 - 32 * 12;
@@ -677,16 +637,6 @@ void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStrea
   a.chains = p.chains;
   a.val = val;
   a.old = old;
-  static const int exp_env = std::getenv("CHROMA_CLUSTER_EXP") ? std::atoi(std::getenv("CHROMA_CLUSTER_EXP")) : 0;
-  a.exp = exp_env;
-  static const bool trace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
-  DBuf<unsigned long long> dbg;
-  a.dbg = nullptr;
-  if (trace) {
-    dbg.alloc(8, s);
-    dbg.zero(s);
-    a.dbg = dbg.p;
-  }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -702,15 +652,6 @@ void launch_gs_cluster(const ClusterPlan& p, i32* val, const i32* old, cudaStrea
   CUDA_CHECK(cudaLaunchKernelEx(&cfg, cluster_kernel(p.DW), a));
   count_launch();
   CUDA_CHECK(cudaGetLastError());
-  if (trace) {
-    unsigned long long h[8];
-    CUDA_CHECK(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    std::fprintf(stderr,
-                 "[cluster] CTA0 cycles: wait %llu colour %llu cluster-sync %llu issue %llu over %llu items, %lld "
-                 "levels; start %llu loop %llu end %llu\n",
-                 h[0], h[1], h[2], h[7], h[3], (long long)p.L, h[4], h[5], h[6]);
-  }
 }
 
 }  // namespace chroma

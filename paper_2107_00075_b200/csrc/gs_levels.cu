@@ -289,11 +289,7 @@ int G(i64 n) { return grid_for(std::max<i64>(n, 1), 256, num_sms() * 16); }
 
 bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl, i64 nwl, DBuf<i32>& out,
                        i64& nout, cudaStream_t s, std::vector<i64>* sizes_out, i64 min_width_override, bool chains) {
-  static const i64 min_width_env = [] {
-    const char* e = std::getenv("CHROMA_LEVEL_MIN_WIDTH");
-    return e ? std::atoll(e) : 2048ll;
-  }();
-  const i64 min_width = min_width_override > 0 ? min_width_override : min_width_env;
+  const i64 min_width = min_width_override > 0 ? min_width_override : 2048;
   static const bool trace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
   if (nwl < 4096) return false;
   const i64 max_levels = nwl / min_width;
@@ -344,8 +340,7 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
   CUDA_CHECK(cudaMemsetAsync(cnt.p + 1, 0, 2 * sizeof(unsigned long long), s));
   i64 lvl = 0;
   bool done = false;
-  static const int grid_mult = std::getenv("CHROMA_LEVEL_GRID") ? std::atoi(std::getenv("CHROMA_LEVEL_GRID")) : 8;
-  const int grid = num_sms() * grid_mult;
+  const int grid = num_sms() * 8;
   while (!done) {
     for (int k = 0; k < BATCH; k++, lvl++) {
       const int p = (int)(lvl & 1);

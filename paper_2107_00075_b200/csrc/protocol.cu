@@ -140,8 +140,6 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     static const i64 heavy_deg = env_i64("CHROMA_FREE_HEAVY", 4096);
     static const i64 rank_cap = env_i64("CHROMA_FREE_RANKCAP", 0);
     static const bool trace = std::getenv("CHROMA_FREE_TRACE") != nullptr;
-    static const bool no_waves = std::getenv("CHROMA_FREE_NOWAVES") != nullptr;
-    static const bool always_spec = std::getenv("CHROMA_FREE_SPECULATE") != nullptr;
     if (ev_k0) CUDA_CHECK(cudaEventRecord(ev_k0, s));
     static const i64 tiny_deg = env_i64("CHROMA_FREE_TINY", 32);
     static const i64 tail_n = env_i64("CHROMA_FREE_TAIL", 4096);
@@ -150,7 +148,7 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
     i64 cnt[6];
     CUDA_CHECK(cudaMemcpyAsync(cnt, S.fcnt.p, 3 * sizeof(i64), cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
-    if (dist == 1 && cnt[1] == 0 && !always_spec && !S.keep_free) {  // no heavy rows
+    if (dist == 1 && cnt[1] == 0 && !S.keep_free) {  // no heavy rows
       algo = CHROMA_ALGO_GAUSS_SEIDEL;
       goto gauss_seidel;
     }
@@ -178,7 +176,7 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
         return;
       }
     }
-    if (cnt[1] > 0 && !no_waves) {
+    if (cnt[1] > 0) {
       const auto tw0 = std::chrono::steady_clock::now();
       const i64 nh = cnt[1];
       launch_free_heavy(rowptr, col, cur, f.heavy[0], cnt[1], f.light[0], f.cnt, dist, partial, S.fw, s);
@@ -205,7 +203,7 @@ void color_csr(const i64* rowptr, const i32* col, i64 nv, i32* colors, const i32
         tl = tn;
       }
       const i64 pend = cnt[3 * q] + cnt[3 * q + 1] + cnt[3 * q + 2];
-      if (pend > 0 && it + 1 >= tail_after && pend <= tail_n && !no_waves) {
+      if (pend > 0 && it + 1 >= tail_after && pend <= tail_n) {
         // a small remainder that keeps colliding is a dense cluster: finish it
         // exactly with the wave kernel instead of iterating one layer at a time
         i32* dst = f.heavy[q];

@@ -475,16 +475,11 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
     DBuf<i32> gcol;
     gcol.alloc(std::max<i64>(nnz, 1), s);
     {
-      const i64 CH = (i64)1 << 26;
-      DBuf<i64> tmp;
-      tmp.alloc(std::min<i64>(std::max<i64>(nnz, 1), CH), s);
-      auto upload = [&](i64 e0, i64 e1) {  // columns [e0, e1), converted to int32 in place
-        for (i64 b = e0; b < e1; b += CH) {
-          const i64 k = std::min(CH, e1 - b);
-          CUDA_CHECK(cudaMemcpyAsync(tmp.p, h_col + b, sizeof(i64) * k, cudaMemcpyHostToDevice, s));
-          k_i64_to_i32<<<G(k), 256, 0, s>>>(tmp.p, gcol.p + b, k);
-          count_launch();
-        }
+      // columns [e0, e1) -> int32, range-checked on the device (ValueError like
+      // chroma_csr_create): later window steps index the host row offsets with
+      // column values read back from the device
+      auto upload = [&](i64 e0, i64 e1) {
+        if (e1 > e0) narrow_ids_checked(h_col + e0, e1 - e0, n, false, gcol.p + e0, s, "col_indices out of range");
       };
       // The builder reads the rows of the owned, layer-1 and (two layers) layer-2
       // vertices only.  When the owned gids of [lo, hi) are one contiguous range (block

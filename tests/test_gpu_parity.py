@@ -373,3 +373,37 @@ def test_select_kernel_picks_edge_based_above_threshold():
             (L.Kernel.EDGE_BASED if thr == 5 else L.Kernel.VERTEX_BASED)
         out.append(R.run_distributed(w, R.AlgorithmConfig(kernel=L.KernelChoice(max_degree_threshold=thr)))[0])
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("gl", [1, 2])
+@pytest.mark.parametrize("part", ["block", "random", "strided"])
+def test_single_rank_world_matches_full_build(gl, part):
+    """A world holding one rank (the one-process-per-GPU form; windowed column upload
+    for contiguous ownership) has exactly the local graph the all-ranks build gives
+    that rank -- block, random and strided ownership, ranks with and without ghosts."""
+    g = G.gen_rmat(12, 8, 5)
+    P = 4
+    if part == "block":
+        pm = PT.partition_block(g, P)
+    elif part == "random":
+        pm = PT.partition_random(g, P, 3)
+    else:
+        pm = PT.PartitionMap((np.arange(g.num_vertices) % P).astype(np.int32), P)
+    full = RT.build_local_graphs(g, pm, gl)
+    for r in range(P):
+        wh = RT.WorldHandle(g, pm, gl, r, r + 1)
+        lg = RT.LocalGraph(wh, r, gl)
+        ref = full.local_graphs[r]
+        for name in ("row_offsets", "col_indices", "gids", "ghost_owner", "boundary_d1", "boundary_d2"):
+            assert np.array_equal(getattr(lg, name), getattr(ref, name)), (part, gl, r, name)
+        assert (lg.owned_count, lg.ghost_count, lg.num_local_edges, lg.num_ghost_edges) == \
+            (ref.owned_count, ref.ghost_count, ref.num_local_edges, ref.num_ghost_edges)
+
+
+def test_world_create_rejects_out_of_range_columns():
+    g = G.gen_hex_mesh(8, 8, 1)
+    bad = G.Graph(g.num_vertices, g.row_offsets.copy(), g.col_indices.copy())
+    bad.col_indices[5] = g.num_vertices + 7
+    for P, lo, hi in ((1, 0, 1), (2, 0, 1)):
+        with pytest.raises(ValueError):
+            RT.WorldHandle(bad, PT.partition_block(bad, P), 1, lo, hi)
