@@ -45,10 +45,10 @@ constexpr i64 CF_TINY = 32;           // rows up to this length: one lane
 constexpr i64 CF_HEAVY = 4096;        // rows longer than this: one CTA
 constexpr int CF_HDR = 4;             // pool record: [k0, k1, nw, nopen | bitmap words | open lids]
 constexpr int CF_OPEN = 128;          // open intra members listed per long row (more: walk the segment)
+constexpr i64 CF_SLICE = 32768;       // a hub row is scanned by ceil(len / CF_SLICE) CTAs
 constexpr u32 OPEN_WALK = 0xffffffffu;
 constexpr unsigned FULLM = 0xffffffffu;
 constexpr int CF_HUBW = 2;            // warps per CTA that resolve open hub rows
-constexpr int CF_HUBMAX = 16;         // hubs of one chunk per hub warp
 
 struct CfArgs {
   const i64* rowptr;
@@ -58,7 +58,13 @@ struct CfArgs {
   const i32* wl;        // sorted unique worklist
   i64 nwl, chunk;
   bool upper_zero;      // every neighbour above a member contributes colour 0
-  i32* big[2];          // first pass: warp / CTA rows of the chunk
+  i32* big[2];          // first pass: warp rows / CTA row slices of the chunk
+  int2* slice;          // per CTA item: (hub slot, slice index)
+  // per hub row (slot): colour bitmap, [intra, nlt0, nltv, slices left, open count], open lids
+  u32* hub_bm;
+  int* hub_cnt;
+  i32* hub_open;
+  unsigned* hub_top;    // next free slot
   unsigned* cnt;        // [0..1] big counts (even chunks), [2] overflow, [3..4] big counts (odd chunks)
   u32* pool;
   unsigned long long* pool_top;
@@ -148,8 +154,11 @@ struct RowScan {
 // a row scanned by `nthreads` cooperating threads (a warp, or a CTA when cta) into
 // the shared bitmap bm; stops after the step that reached entries above v
 __device__ void first_scan(const CfArgs& a, i32 v, i32 s0, int tid, int nthreads, bool cta, u32* bm,
-                           RowScan& out, i32* olist, int* on) {
-  const i64 rs = a.rowptr[v], re = a.rowptr[v + 1];
+                           RowScan& out, i32* olist, int* on, i64 rs = -1, i64 re = -1) {
+  if (rs < 0) {
+    rs = a.rowptr[v];
+    re = a.rowptr[v + 1];
+  }
   int intra = 0, nlt0 = 0, nltv = 0;
   for (i64 j = rs; j < re; j += (i64)nthreads * 4) {
     i32 us[4];
@@ -358,7 +367,7 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
     unsigned* const bc = a.cnt + (((a0 / a.chunk) & 1) ? 3 : 0);
     unsigned* const bc_next = a.cnt + (((a0 / a.chunk) & 1) ? 0 : 3);
     const i64 a1 = a0 + a.chunk < a.nwl ? a0 + a.chunk : a.nwl;
-    const i32 s0 = a.wl[a0], s1 = a.wl[a1 - 1];
+    const i32 s0 = a.wl[a0];
     const i64 ngroups = (a1 - a0 + 31) / 32;
     // ---------------- first pass (1): lanes take short rows; longer rows are listed
     for (i64 g = gw; g < ngroups; g += nwarps) {
@@ -366,15 +375,30 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
       const i32 v = p < a1 ? a.wl[p] : -1;
       const i64 deg = v >= 0 ? a.rowptr[v + 1] - a.rowptr[v] : 0;
       if (v >= 0 && deg <= CF_TINY) first_lane(a, v, s0);
-#pragma unroll
-      for (int k = 0; k < 2; k++) {
-        const bool mine = v >= 0 && (k == 0 ? (deg > CF_TINY && deg <= CF_HEAVY) : deg > CF_HEAVY);
+      {
+        const bool mine = v >= 0 && deg > CF_TINY && deg <= CF_HEAVY;
         const unsigned b = __ballot_sync(FULLM, mine);
-        if (!b) continue;
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(bc + k, (unsigned)__popc(b));
-        base = __shfl_sync(FULLM, base, 0);
-        if (mine) a.big[k][base + __popc(b & ((1u << lane) - 1u))] = v;
+        if (b) {
+          unsigned base = 0;
+          if (lane == 0) base = atomicAdd(bc, (unsigned)__popc(b));
+          base = __shfl_sync(FULLM, base, 0);
+          if (mine) a.big[0][base + __popc(b & ((1u << lane) - 1u))] = v;
+        }
+      }
+      if (v >= 0 && deg > CF_HEAVY) {  // a hub: one accumulator slot, one item per slice
+        const int nsl = (int)((deg + CF_SLICE - 1) / CF_SLICE);
+        const unsigned slot = atomicAdd(a.hub_top, 1u);
+        const unsigned base = atomicAdd(bc + 1, (unsigned)nsl);
+        u32* hb = a.hub_bm + (i64)slot * CF_WORDS;
+        for (int w = 0; w < CF_WORDS; w++) hb[w] = 0;
+        int* hc = a.hub_cnt + (i64)slot * 8;
+        hc[0] = hc[1] = hc[2] = 0;
+        hc[3] = nsl;
+        hc[4] = 0;
+        for (int j = 0; j < nsl; j++) {
+          a.big[1][base + j] = v;
+          a.slice[base + j] = make_int2((int)slot, j);
+        }
       }
     }
     grid.sync();
@@ -383,13 +407,19 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
     {
       // lists and counts written by other SMs before the barrier: read at L2
       const unsigned nc = __ldcg(bc + 1), nwr = __ldcg(bc + 0);
+      // hub rows: every slice by one CTA; partial results meet in the hub's slot and
+      // the CTA that finishes the last slice finishes the row
+      __shared__ int last;
       for (unsigned h = blockIdx.x; h < nc; h += gridDim.x) {
         const i32 vh = __ldcg(a.big[1] + h);
+        const int2 it = __ldcg(a.slice + h);
+        const i64 rs = a.rowptr[vh], re = a.rowptr[vh + 1];
+        const i64 b0 = rs + (i64)it.y * CF_SLICE, b1 = b0 + CF_SLICE < re ? b0 + CF_SLICE : re;
         if (threadIdx.x < CF_WORDS) cbm[threadIdx.x] = 0;
         if (threadIdx.x == 0) clen = 0;
         __syncthreads();
         RowScan r;
-        first_scan(a, vh, s0, threadIdx.x, CF_THREADS, true, cbm, r, clist, &clen);
+        first_scan(a, vh, s0, threadIdx.x, CF_THREADS, true, cbm, r, clist, &clen, b0, b1);
         r.intra = __reduce_add_sync(FULLM, r.intra);
         r.nlt0 = __reduce_add_sync(FULLM, r.nlt0);
         r.nltv = __reduce_add_sync(FULLM, r.nltv);
@@ -399,12 +429,38 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
           cred[2][wid] = r.nltv;
         }
         __syncthreads();
+        u32* hb = a.hub_bm + (i64)it.x * CF_WORDS;
+        int* hc = a.hub_cnt + (i64)it.x * 8;
+        i32* ho = a.hub_open + (i64)it.x * CF_OPEN;
         if (wid == 0) {
           RowScan t{cred[0][lane], cred[1][lane], cred[2][lane]};
           t.intra = __reduce_add_sync(FULLM, t.intra);
           t.nlt0 = __reduce_add_sync(FULLM, t.nlt0);
           t.nltv = __reduce_add_sync(FULLM, t.nltv);
-          first_finish(a, vh, t, cbm, lane, clist, clen);
+          if (cbm[lane]) atomicOr(hb + lane, cbm[lane]);
+          const int nl = clen < CF_OPEN ? clen : CF_OPEN;
+          int base = 0;
+          if (lane == 0) {
+            atomicAdd(hc + 0, t.intra);
+            atomicAdd(hc + 1, t.nlt0);
+            atomicAdd(hc + 2, t.nltv);
+            base = atomicAdd(hc + 4, clen);  // > CF_OPEN in total: the resolver walks the segment
+          }
+          base = __shfl_sync(FULLM, base, 0);
+          for (int k = lane; k < nl && base + k < CF_OPEN; k += 32) ho[base + k] = clist[k];
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) last = atomicSub(hc + 3, 1) == 1;
+        }
+        __syncthreads();
+        if (last && wid == 0) {  // every slice is in: finish the row from the slot
+          __threadfence();
+          cbm[lane] = __ldcg(hb + lane);
+          const int nopen = __ldcg(hc + 4);
+          for (int k = lane; k < CF_OPEN && k < nopen; k += 32) clist[k] = __ldcg(ho + k);
+          __syncwarp();
+          const RowScan t{__ldcg(hc + 0), __ldcg(hc + 1), __ldcg(hc + 2)};
+          first_finish(a, vh, t, cbm, lane, clist, nopen);
         }
         __syncthreads();
       }
@@ -492,7 +548,20 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   const i64 nchunks = nchunks_env > 0 ? nchunks_env : 32;
   i64 chunk = std::max<i64>((i64)1 << 15, (nwl + nchunks - 1) / nchunks);
   if (chunk > nwl) chunk = nwl;
-  S.heavy.reserve(2 * chunk, s);
+  // hub rows (deg > CF_HEAVY, so at most nnz / CF_HEAVY of them): one accumulator slot
+  // each; their slices (<= deg / CF_SLICE + 1 per hub) are the chunk's CTA items
+  i64 nnz_all = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&nnz_all, L.rowptr + nv, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  const i64 hub_cap = nnz_all / CF_HEAVY + 2;
+  const i64 item_cap = chunk + nnz_all / CF_SLICE + 2;
+  S.heavy.reserve(chunk + item_cap, s);
+  S.slice.reserve(item_cap, s);
+  S.hub_bm.reserve(hub_cap * CF_WORDS, s);
+  S.hub_cnt.reserve(hub_cap * 8, s);
+  S.hub_open.reserve(hub_cap * CF_OPEN, s);
+  S.hub_top.reserve(1, s);
+  CUDA_CHECK(cudaMemsetAsync(S.hub_top.p, 0, sizeof(unsigned), s));
   S.cnt.reserve(8, s);
   S.cnt.zero(s);
   S.desc.reserve(nv, s);
@@ -515,6 +584,11 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   a.upper_zero = upper_zero && L.old == nullptr;
   a.big[0] = S.heavy.p;
   a.big[1] = S.heavy.p + chunk;
+  a.slice = S.slice.p;
+  a.hub_bm = S.hub_bm.p;
+  a.hub_cnt = S.hub_cnt.p;
+  a.hub_open = S.hub_open.p;
+  a.hub_top = S.hub_top.p;
   a.cnt = S.cnt.p;
   a.pool = S.pool.p;
   a.pool_top = S.pool_top.p;

@@ -30,8 +30,10 @@ void launch_gs(const GsLaunch& L, cudaStream_t s);
 // worklist length.  false: a colour above 1024 appeared, the worklist is back at
 // PENDING and the caller takes launch_gs.
 struct ChunkedScratch {
-  DBuf<u32> pool;
-  DBuf<i32> heavy, iota, flag;
+  DBuf<u32> pool, hub_bm;
+  DBuf<i32> heavy, iota, flag, hub_cnt, hub_open;
+  DBuf<int2> slice;
+  DBuf<unsigned> hub_top;
   DBuf<unsigned> cnt;
   DBuf<u32> desc;
   DBuf<unsigned long long> pool_top;

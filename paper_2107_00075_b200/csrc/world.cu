@@ -93,10 +93,6 @@ __global__ void k_scatter_pos(const i32* list, i64 k, i32* pos) {
     pos[list[i]] = (i32)i;
 }
 
-__global__ void k_i64_to_i32(const i64* in, i32* out, i64 n) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
-    out[i] = (i32)in[i];
-}
 
 // out[0] = min, out[1] = max, out[2] = count of the gids owned by ranks [lo, hi)
 __global__ void k_owned_range(const i32* owner, i64 n, i32 lo, i32 hi, unsigned long long* out) {
