@@ -119,7 +119,7 @@ int chroma_csr_create(int64_t n, const int64_t* off, const int64_t* col, int dev
         h->g.rowptr.alloc(n + 1, s);
         CUDA_CHECK(cudaMemcpyAsync(h->g.rowptr.p, off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, s));
       } else {
-        h->g.rowptr.upload(off, n + 1, s);
+        upload_large(h->g.rowptr, off, n + 1, s);
       }
       i64 nnz = 0;
       CUDA_CHECK(cudaMemcpyAsync(&nnz, h->g.rowptr.p + n, sizeof(i64), cudaMemcpyDeviceToHost, s));
@@ -127,7 +127,7 @@ int chroma_csr_create(int64_t n, const int64_t* off, const int64_t* col, int dev
       CHROMA_REQUIRE(nnz >= 0, CHROMA_EVALUE, "row_offsets[n] must be >= 0");
       h->g.n = n;
       h->g.nnz = nnz;
-      // narrowed and range-checked on the device (no host pass over the columns)
+      // narrowed and range-checked on the way in (upload.cu for host arrays)
       h->g.col.alloc(std::max<i64>(nnz, 1), s);
       narrow_ids_checked(col, nnz, n, dev(flags), h->g.col.p, s, "col_indices out of range");
       CUDA_CHECK(cudaStreamSynchronize(s));

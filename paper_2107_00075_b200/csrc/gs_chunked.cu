@@ -9,8 +9,8 @@
 // the hub rows (920 ms on C3, R-MAT scale 24).  Here W is cut into position chunks
 // of B vertices, processed in order:
 //   * first pass (throughput): every member v of the chunk scans the lower part of
-//     its row once -- a lane for rows of <= 32 entries, a warp up to 4096, a CTA
-//     beyond.  Neighbours outside the chunk and chunk members that are already
+//     its row once -- a lane for rows of <= 32 entries, 8 lanes up to 256, a warp
+//     up to 4096, CTAs (32k-entry slices) beyond.  Neighbours outside the chunk and chunk members that are already
 //     final form v's external colour set.  If no smaller chunk member is still open,
 //     v is final at once: mex(external), ~90 % of the vertices.  Otherwise v stays
 //     open and its external set is kept as a bitmap record (pool).
@@ -58,14 +58,15 @@ struct CfArgs {
   const i32* wl;        // sorted unique worklist
   i64 nwl, chunk;
   bool upper_zero;      // every neighbour above a member contributes colour 0
-  i32* big[2];          // first pass: warp rows / CTA row slices of the chunk
+  i32* big[3];          // first pass: warp rows / CTA row slices / group rows of the chunk
   int2* slice;          // per CTA item: (hub slot, slice index)
   // per hub row (slot): colour bitmap, [intra, nlt0, nltv, slices left, open count], open lids
   u32* hub_bm;
   int* hub_cnt;
   i32* hub_open;
   unsigned* hub_top;    // next free slot
-  unsigned* cnt;        // [0..1] big counts (even chunks), [2] overflow, [3..4] big counts (odd chunks)
+  unsigned* cnt;        // [0..2] big counts (even chunks), [3..5] (odd chunks), [6] overflow
+  i64 med;              // rows of CF_TINY < deg <= med: one 8-lane group (first pass)
   u32* pool;
   unsigned long long* pool_top;
   u32* desc;            // per vertex: pool offset of its record
@@ -151,10 +152,10 @@ __device__ void first_lane(const CfArgs& a, i32 v, i32 s0) {
 struct RowScan {
   int intra, nlt0, nltv;
 };
-// a row scanned by `nthreads` cooperating threads (a warp, or a CTA when cta) into
+// a row scanned by `nthreads` cooperating threads (lanes gm of a warp, or a CTA when cta) into
 // the shared bitmap bm; stops after the step that reached entries above v
 __device__ void first_scan(const CfArgs& a, i32 v, i32 s0, int tid, int nthreads, bool cta, u32* bm,
-                           RowScan& out, i32* olist, int* on, i64 rs = -1, i64 re = -1) {
+                           RowScan& out, i32* olist, int* on, i64 rs = -1, i64 re = -1, unsigned gm = FULLM) {
   if (rs < 0) {
     rs = a.rowptr[v];
     re = a.rowptr[v + 1];
@@ -187,7 +188,7 @@ __device__ void first_scan(const CfArgs& a, i32 v, i32 s0, int tid, int nthreads
       }
       if (c >= 1 && c <= CF_WORDS * 32) atomicOr(bm + ((c - 1) >> 5), 1u << ((c - 1) & 31));
     }
-    const bool any = cta ? __syncthreads_or(above) : __any_sync(FULLM, above);
+    const bool any = cta ? __syncthreads_or(above) : __any_sync(gm, above);
     if (any) break;
   }
   out = {intra, nlt0, nltv};
@@ -203,25 +204,38 @@ __device__ __forceinline__ i32 warp_mex(const u32* bm, int lane) {
   return l * 32 + __ffs(~wl);
 }
 
-// finish a cooperative first pass (one warp)
-__device__ void first_finish(const CfArgs& a, i32 v, const RowScan& r, const u32* bm, int lane, const i32* olist,
-                             int nopen) {
-  const i32 t = warp_mex(bm, lane);
+// first zero bit of bm[0..32) by the G lanes gm of a warp (gl: lane in the group); 0 if full
+template <int G>
+__device__ __forceinline__ i32 group_mex(const u32* bm, int gl, unsigned gm) {
+  constexpr int PER = 32 / G;
+  int wi = 32;
+#pragma unroll
+  for (int k = PER - 1; k >= 0; k--)
+    if (bm[gl * PER + k] != FULLM) wi = gl * PER + k;
+  wi = (int)__reduce_min_sync(gm, (unsigned)wi);
+  return wi == 32 ? 0 : wi * 32 + __ffs(~bm[wi]);
+}
+
+// finish a cooperative first pass (G lanes gm of a warp, led by lane `lead`)
+template <int G>
+__device__ void first_finish(const CfArgs& a, i32 v, const RowScan& r, const u32* bm, int gl, unsigned gm, int lead,
+                             const i32* olist, int nopen) {
+  const i32 t = group_mex<G>(bm, gl, gm);
   if (t == 0) {  // more than 1024 colours: publish anything (no waiter may hang), fall back
-    if (lane == 0) {
-      atomicOr(a.cnt + 2, 1u);
+    if (gl == 0) {
+      atomicOr(a.cnt + 6, 1u);
       publish(a, v, 1);
     }
     return;
   }
   if (r.intra == 0) {
-    if (lane == 0) publish(a, v, t);
+    if (gl == 0) publish(a, v, t);
     return;
   }
   const int nw = words_for(a.rowptr[v + 1] - a.rowptr[v]);
   const bool listed = nopen <= CF_OPEN;
   u32 off = 0;
-  if (lane == 0) {
+  if (gl == 0) {
     off = pool_alloc(a, nw + (listed ? nopen : 0));
     u32* rec = a.pool + off;
     rec[0] = (u32)r.nlt0;
@@ -230,10 +244,10 @@ __device__ void first_finish(const CfArgs& a, i32 v, const RowScan& r, const u32
     rec[3] = listed ? (u32)nopen : OPEN_WALK;
     a.desc[v] = off;
   }
-  off = __shfl_sync(FULLM, off, 0);
-  if (lane < nw) a.pool[off + CF_HDR + lane] = bm[lane];
+  off = __shfl_sync(gm, off, lead);
+  for (int w = gl; w < nw; w += G) a.pool[off + CF_HDR + w] = bm[w];
   if (listed)
-    for (int k = lane; k < nopen; k += 32) a.pool[off + CF_HDR + nw + k] = (u32)olist[k];
+    for (int k = gl; k < nopen; k += G) a.pool[off + CF_HDR + nw + k] = (u32)olist[k];
 }
 
 // ------------------------------------------------------------------ dataflow
@@ -284,7 +298,7 @@ __device__ void resolve_lane(const CfArgs& a, i32 v, u32* lbm) {
     if (x != FULLM) t = w * 32 + __ffs(~x);
   }
   if (t == 0) {
-    atomicOr(a.cnt + 2, 1u);
+    atomicOr(a.cnt + 6, 1u);
     t = 1;
   }
   publish(a, v, t);
@@ -310,7 +324,7 @@ __device__ void resolve_warp(const CfArgs& a, i32 v, u32* bm, int lane) {
     __syncwarp();
     const i32 t = warp_mex(bm, lane);
     if (lane == 0) {
-      if (t == 0) atomicOr(a.cnt + 2, 1u);
+      if (t == 0) atomicOr(a.cnt + 6, 1u);
       publish(a, v, t == 0 ? 1 : t);
     }
     __syncwarp();
@@ -333,7 +347,7 @@ __device__ void resolve_warp(const CfArgs& a, i32 v, u32* bm, int lane) {
   __syncwarp();
   const i32 t = warp_mex(bm, lane);
   if (lane == 0) {
-    if (t == 0) atomicOr(a.cnt + 2, 1u);
+    if (t == 0) atomicOr(a.cnt + 6, 1u);
     publish(a, v, t == 0 ? 1 : t);
   }
   __syncwarp();
@@ -347,7 +361,7 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
   __shared__ int cred[3][CF_WARPS];
   __shared__ i32 wlist[CF_WARPS][CF_OPEN];  // open intra members of a long row (first pass)
   __shared__ i32 clist[CF_OPEN];
-  __shared__ int wlen[CF_WARPS], clen;
+  __shared__ int wlen[CF_WARPS], clen, glen[CF_WARPS * 4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u32* bm = wbm[wid];
   const i64 gw = (i64)blockIdx.x * CF_WARPS + wid, nwarps = (i64)gridDim.x * CF_WARPS;
@@ -376,13 +390,17 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
       const i64 deg = v >= 0 ? a.rowptr[v + 1] - a.rowptr[v] : 0;
       if (v >= 0 && deg <= CF_TINY) first_lane(a, v, s0);
       {
-        const bool mine = v >= 0 && deg > CF_TINY && deg <= CF_HEAVY;
-        const unsigned b = __ballot_sync(FULLM, mine);
-        if (b) {
-          unsigned base = 0;
-          if (lane == 0) base = atomicAdd(bc, (unsigned)__popc(b));
-          base = __shfl_sync(FULLM, base, 0);
-          if (mine) a.big[0][base + __popc(b & ((1u << lane) - 1u))] = v;
+        // warp rows (list 0) and group rows (list 2)
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          const bool mine = v >= 0 && deg > CF_TINY && deg <= CF_HEAVY && (deg <= a.med) == (q == 1);
+          const unsigned b = __ballot_sync(FULLM, mine);
+          if (b) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(bc + 2 * q, (unsigned)__popc(b));
+            base = __shfl_sync(FULLM, base, 0);
+            if (mine) a.big[2 * q][base + __popc(b & ((1u << lane) - 1u))] = v;
+          }
         }
       }
       if (v >= 0 && deg > CF_HEAVY) {  // a hub: one accumulator slot, one item per slice
@@ -460,7 +478,7 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
           for (int k = lane; k < CF_OPEN && k < nopen; k += 32) clist[k] = __ldcg(ho + k);
           __syncwarp();
           const RowScan t{__ldcg(hc + 0), __ldcg(hc + 1), __ldcg(hc + 2)};
-          first_finish(a, vh, t, cbm, lane, clist, nopen);
+          first_finish<32>(a, vh, t, cbm, lane, FULLM, 0, clist, nopen);
         }
         __syncthreads();
       }
@@ -475,15 +493,42 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
         r.nlt0 = __reduce_add_sync(FULLM, r.nlt0);
         r.nltv = __reduce_add_sync(FULLM, r.nltv);
         __syncwarp();
+        first_finish<32>(a, vl, r, bm, lane, FULLM, 0, wlist[wid], wlen[wid]);
         __syncwarp();
-        first_finish(a, vl, r, bm, lane, wlist[wid], wlen[wid]);
-        __syncwarp();
+      }
+      // group rows: four per warp, 8 lanes each; bitmaps and open lists in the
+      // resolvers' shared memory, which the first pass does not use
+      {
+        constexpr int G = 8, NG = 32 / G;
+        const unsigned nmed = __ldcg(bc + 2);
+        const int g = lane / G, gl = lane % G;
+        const unsigned gm = ((1u << G) - 1u) << (g * G);
+        const int slot = wid * NG + g;
+        u32* gbm = lbm_all + slot * CF_WORDS;
+        i32* glist = (i32*)lbm_all + CF_WARPS * NG * CF_WORDS + slot * CF_OPEN;
+        for (i64 h0 = gw * NG; h0 < nmed; h0 += nwarps * NG) {
+          const i64 h = h0 + g;
+          if (h < nmed) {
+            const i32 vm = __ldcg(a.big[2] + h);
+            for (int w = gl; w < CF_WORDS; w += G) gbm[w] = 0;
+            if (gl == 0) glen[slot] = 0;
+            __syncwarp(gm);
+            RowScan r;
+            first_scan(a, vm, s0, gl, G, false, gbm, r, glist, &glen[slot], -1, -1, gm);
+            r.intra = __reduce_add_sync(gm, r.intra);
+            r.nlt0 = __reduce_add_sync(gm, r.nlt0);
+            r.nltv = __reduce_add_sync(gm, r.nltv);
+            __syncwarp(gm);
+            first_finish<G>(a, vm, r, gbm, gl, gm, g * G, glist, glen[slot]);
+            __syncwarp(gm);
+          }
+        }
       }
     }
     grid.sync();
     tr(2, 0);
     // ---------------- dataflow over the open vertices
-    if (blockIdx.x == 0 && threadIdx.x < 2) bc_next[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < 3) bc_next[threadIdx.x] = 0;
     if (wid < CF_HUBW) {
       // hub warps: this warp's hubs of the chunk, ascending
       const unsigned nh = __ldcg(bc + 1);
@@ -496,7 +541,7 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
         nm++;
       }
       if (nm > 32) {
-        if (lane == 0) atomicOr(a.cnt + 2, 1u);  // cannot happen below 4,736 hubs per chunk
+        if (lane == 0) atomicOr(a.cnt + 6, 1u);  // cannot happen below 4,736 hubs per chunk
         nm = 32;
       }
       for (int k = 0; k < nm; k++) {
@@ -541,6 +586,10 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
     launch_iota_i32(S.iota.p, nwl, (i32)L.wl_base, s);
     wl = S.iota.p;
   }
+  static const i64 med = [] {
+    const char* e = std::getenv("CHROMA_GS_MED");
+    return e ? std::atoll(e) : (i64)256;
+  }();
   static const i64 nchunks_env = [] {
     const char* e = std::getenv("CHROMA_GS_CHUNKS");
     return e ? std::atoll(e) : 0;
@@ -555,7 +604,7 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   CUDA_CHECK(cudaStreamSynchronize(s));
   const i64 hub_cap = nnz_all / CF_HEAVY + 2;
   const i64 item_cap = chunk + nnz_all / CF_SLICE + 2;
-  S.heavy.reserve(chunk + item_cap, s);
+  S.heavy.reserve(2 * chunk + item_cap, s);
   S.slice.reserve(item_cap, s);
   S.hub_bm.reserve(hub_cap * CF_WORDS, s);
   S.hub_cnt.reserve(hub_cap * 8, s);
@@ -565,9 +614,7 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   S.cnt.reserve(8, s);
   S.cnt.zero(s);
   S.desc.reserve(nv, s);
-  i64 nnz = 0;
-  CUDA_CHECK(cudaMemcpyAsync(&nnz, L.rowptr + nv, sizeof(i64), cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
+  const i64 nnz = nnz_all;
   // bitmaps (<= deg/32 + 2 words), headers, and open lids (<= intra entries <= nnz)
   const i64 pool_words = nnz / 32 + (i64)(CF_HDR + 4) * nwl + std::min<i64>(nnz, (i64)CF_OPEN * nwl) + 4096;
   S.pool.reserve(pool_words, s);
@@ -584,6 +631,8 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   a.upper_zero = upper_zero && L.old == nullptr;
   a.big[0] = S.heavy.p;
   a.big[1] = S.heavy.p + chunk;
+  a.big[2] = S.heavy.p + chunk + item_cap;
+  a.med = med;
   a.slice = S.slice.p;
   a.hub_bm = S.hub_bm.p;
   a.hub_cnt = S.hub_cnt.p;
@@ -627,7 +676,7 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
                  (long long)nwl, (long long)chunk, ph_t[1] * 1e-3, ph_t[2] * 1e-3, ph_t[3] * 1e-3);
   }
   unsigned ovf = 0;
-  CUDA_CHECK(cudaMemcpyAsync(&ovf, S.cnt.p + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaMemcpyAsync(&ovf, S.cnt.p + 6, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
   if (ovf) {
     launch_scatter_const(L.val, wl, L.nwl_dev, nwl, PENDING, s);

@@ -124,6 +124,21 @@ void select_flagged_values(const i32* values, const uint8_t* flags, i64 n, i32* 
                            cudaStream_t s);
 void exclusive_scan_i64(const i64* in, i64* out, i64 n, cudaStream_t s);
 i64 unique_u64(const u64* in, i64 n, u64* out, cudaStream_t s);  // sorted input; returns count
+// host -> device through the pinned staging ring (upload.cu); large arrays only
+bool staged_upload_wanted(i64 bytes);
+void upload_narrow_host(const i64* src, i64 k, i64 n, i32* out, cudaStream_t s, const char* what);
+void upload_bytes_host(const void* src, i64 bytes, void* out, cudaStream_t s);
+// DBuf::upload for large host arrays (staged when that pays)
+template <typename T>
+void upload_large(DBuf<T>& b, const T* h, i64 count, cudaStream_t s) {
+  const i64 bytes = (i64)sizeof(T) * count;
+  if (!staged_upload_wanted(bytes)) {
+    b.upload(h, count, s);
+    return;
+  }
+  b.alloc(count, s);
+  upload_bytes_host(h, bytes, b.p, s);
+}
 void narrow_ids_checked(const i64* src, i64 k, i64 n, bool src_on_device, i32* out, cudaStream_t s,
                         const char* what);
 void sort_i32(i32* keys, i64 n, cudaStream_t s);  // ascending, in place (non-negative keys)

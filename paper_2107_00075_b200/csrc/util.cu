@@ -207,6 +207,10 @@ __global__ void k_narrow_checked(const i64* in, i32* out, i64 k, i64 n, unsigned
 void narrow_ids_checked(const i64* src, i64 k, i64 n, bool src_on_device, i32* out, cudaStream_t s,
                         const char* what) {
   if (k <= 0) return;
+  if (!src_on_device && staged_upload_wanted(k * (i64)sizeof(i64))) {
+    upload_narrow_host(src, k, n, out, s, what);
+    return;
+  }
   DBuf<unsigned> bad;
   bad.alloc(1, s);
   bad.zero(s);

@@ -441,12 +441,12 @@ World* world_create(i64 n, const i64* h_off, const i64* h_col, i32 P, const i32*
 
     PhaseTimer ptm(s);
     DBuf<i64> goff;
-    goff.upload(h_off, n + 1, s);
+    upload_large(goff, h_off, n + 1, s);
     // owner: uploaded (any PartitionMap) or computed (partition_block when h_owner is NULL);
     // validated on the device (chroma/partition.py:36-43, chroma/runtime.py:159-161)
     DBuf<i32> owner;
     if (h_owner) {
-      owner.upload(h_owner, std::max<i64>(n, 1), s);
+      upload_large(owner, h_owner, std::max<i64>(n, 1), s);
     } else {
       owner.alloc(std::max<i64>(n, 1), s);
       k_block_owner<<<G(n), 256, 0, s>>>(owner.p, n, P);

@@ -91,7 +91,7 @@ class Communicator:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h and _lib._lib is not None:
+        if h and _lib is not None and getattr(_lib, "_lib", None) is not None:
             _lib._lib.chroma_comm_destroy(h)
             self.h = None
 

@@ -51,7 +51,7 @@ class _Comms:
         _lib.check(_lib.lib().chroma_comm_create_all(self.n, arr, self.h), "chroma_comm_create_all")
 
     def __del__(self):
-        if _lib._lib is not None:
+        if _lib is not None and getattr(_lib, "_lib", None) is not None:
             for i in range(self.n):
                 if self.h[i]:
                     _lib._lib.chroma_comm_destroy(self.h[i])

@@ -105,3 +105,31 @@ def test_free_running_within_5pct(key, mode, P):
     assert violations(g, colors, mode) == 0
     ncol = len(np.unique(colors))
     assert ncol <= 1.05 * ref["colors"], (ncol, ref["colors"])
+
+
+def _host_copy(g):
+    """The same graph as plain (pageable) NumPy arrays: the drop-in caller's input."""
+    return G.Graph(g.num_vertices, np.array(g.row_offsets, np.int64), np.array(g.col_indices, np.int64))
+
+
+@pytest.mark.parametrize("P", [1, 8])
+def test_host_arrays_staged_upload_bit_exact(P):
+    # pageable int64 CSR -> staged, narrowed upload (csrc/upload.cu) -> same colours
+    hg = _host_copy(graph("c3_s24"))
+    colors, reports = run(hg, "d1", P)
+    ref = SCALE["c3_s24"][f"d1_p{P}"]
+    assert sha(colors) == ref["sha256"]
+    assert [r.conflicts for r in reports] == ref["conflicts"]
+
+
+def test_host_arrays_serial_greedy_and_range_check():
+    from paper_2107_00075_b200 import localcolor as L
+    hg = _host_copy(graph("c1_1000"))  # 4 M columns: above the staging threshold
+    assert sha(L.serial_greedy(hg)) == SCALE["c1_1000"]["d1_p1"]["sha256"]
+    bad = np.array(hg.col_indices)
+    bad[len(bad) // 2 + 12345] = hg.num_vertices
+    bg = G.Graph(hg.num_vertices, hg.row_offsets, bad)
+    with pytest.raises(ValueError, match="out of range"):
+        RT.build_local_graphs(bg, PT.partition_block(bg, 1), 1)
+    with pytest.raises(ValueError, match="out of range"):
+        L.serial_greedy(bg)
