@@ -45,6 +45,7 @@ constexpr i64 CF_TINY = 32;           // rows up to this length: one lane
 constexpr i64 CF_HEAVY = 4096;        // rows longer than this: one CTA
 constexpr int CF_HDR = 4;             // pool record: [k0, k1, nw, nopen | bitmap words | open lids]
 constexpr int CF_OPEN = 128;          // open intra members listed per long row (more: walk the segment)
+constexpr int CF_HUB_OPEN = 1024;     // ... per hub row
 constexpr i64 CF_SLICE = 32768;       // a hub row is scanned by ceil(len / CF_SLICE) CTAs
 constexpr u32 OPEN_WALK = 0xffffffffu;
 constexpr unsigned FULLM = 0xffffffffu;
@@ -65,6 +66,8 @@ struct CfArgs {
   int* hub_cnt;
   i32* hub_open;
   unsigned* hub_top;    // next free slot
+  unsigned hub_cap;     // slots (more hubs than counted: overflow, the caller falls back)
+  int hub_list;         // open members listed per hub row (<= CF_HUB_OPEN; more: walk)
   unsigned* cnt;        // [0..2] big counts (even chunks), [3..5] (odd chunks), [6] overflow
   i64 med;              // rows of CF_TINY < deg <= med: one 8-lane group (first pass)
   u32* pool;
@@ -155,7 +158,8 @@ struct RowScan {
 // a row scanned by `nthreads` cooperating threads (lanes gm of a warp, or a CTA when cta) into
 // the shared bitmap bm; stops after the step that reached entries above v
 __device__ void first_scan(const CfArgs& a, i32 v, i32 s0, int tid, int nthreads, bool cta, u32* bm,
-                           RowScan& out, i32* olist, int* on, i64 rs = -1, i64 re = -1, unsigned gm = FULLM) {
+                           RowScan& out, i32* olist, int* on, i64 rs = -1, i64 re = -1, unsigned gm = FULLM,
+                           int cap = CF_OPEN) {
   if (rs < 0) {
     rs = a.rowptr[v];
     re = a.rowptr[v + 1];
@@ -184,7 +188,7 @@ __device__ void first_scan(const CfArgs& a, i32 v, i32 s0, int tid, int nthreads
       nltv += u < v;
       if (open) {  // list it (the resolver then waits on these entries only)
         const int k = atomicAdd(on, 1);
-        if (k < CF_OPEN) olist[k] = u;
+        if (k < cap) olist[k] = u;
       }
       if (c >= 1 && c <= CF_WORDS * 32) atomicOr(bm + ((c - 1) >> 5), 1u << ((c - 1) & 31));
     }
@@ -219,7 +223,7 @@ __device__ __forceinline__ i32 group_mex(const u32* bm, int gl, unsigned gm) {
 // finish a cooperative first pass (G lanes gm of a warp, led by lane `lead`)
 template <int G>
 __device__ void first_finish(const CfArgs& a, i32 v, const RowScan& r, const u32* bm, int gl, unsigned gm, int lead,
-                             const i32* olist, int nopen) {
+                             const i32* olist, int nopen, int cap = CF_OPEN) {
   const i32 t = group_mex<G>(bm, gl, gm);
   if (t == 0) {  // more than 1024 colours: publish anything (no waiter may hang), fall back
     if (gl == 0) {
@@ -233,7 +237,7 @@ __device__ void first_finish(const CfArgs& a, i32 v, const RowScan& r, const u32
     return;
   }
   const int nw = words_for(a.rowptr[v + 1] - a.rowptr[v]);
-  const bool listed = nopen <= CF_OPEN;
+  const bool listed = nopen <= cap;
   u32 off = 0;
   if (gl == 0) {
     off = pool_alloc(a, nw + (listed ? nopen : 0));
@@ -273,10 +277,24 @@ __device__ void resolve_lane(const CfArgs& a, i32 v, u32* lbm) {
 #pragma unroll 4
   for (int w = 0; w < CF_WORDS; w++) lbm[w * CF_THREADS] = w < nw ? __ldcg(rec + CF_HDR + w) : 0u;
   const bool listed = nopen != OPEN_WALK && a.rowptr[v + 1] - rs > CF_TINY;
-  for (u32 k = 0; listed && k < nopen; k++) {
-    const i32 x = wait_final(a, (i32)__ldcg(rec + CF_HDR + nw + k));
-    const i32 c = -x - 2;
-    if (c >= 1 && c <= CF_WORDS * 32) lbm[((c - 1) >> 5) * CF_THREADS] |= 1u << ((c - 1) & 31);
+  if (a.trace && !listed && a.rowptr[v + 1] - rs > CF_TINY) {
+    atomicAdd(a.trace + 8190, 1ull);
+    atomicAdd(a.trace + 8191, (unsigned long long)(k1 - k0));
+  }
+  // listed members: 8 loads in flight, spin only on the ones still open
+  for (u32 k = 0; listed && k < nopen; k += 8) {
+    i32 us[8], xs[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) us[q] = k + q < nopen ? (i32)__ldcg(rec + CF_HDR + nw + k + q) : -1;
+#pragma unroll
+    for (int q = 0; q < 8; q++) xs[q] = us[q] >= 0 ? ld_relaxed(a.val + us[q]) : 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      if (us[q] < 0) continue;
+      const i32 x = xs[q] == PENDING ? wait_final(a, us[q]) : xs[q];
+      const i32 c = -x - 2;
+      if (c >= 1 && c <= CF_WORDS * 32) lbm[((c - 1) >> 5) * CF_THREADS] |= 1u << ((c - 1) & 31);
+    }
   }
   for (i64 j = listed ? k1 : k0; j < k1; j += 8) {
     i32 us[8], xs[8];
@@ -313,13 +331,25 @@ __device__ void resolve_warp(const CfArgs& a, i32 v, u32* bm, int lane) {
   const u32 nopen = __ldcg(rec + 3);
   bm[lane] = lane < nw ? __ldcg(rec + CF_HDR + lane) : 0u;
   __syncwarp();
+  if (a.trace && lane == 0) {
+    atomicAdd(a.trace + 8188, 1ull);
+    if (nopen == OPEN_WALK) atomicAdd(a.trace + 8189, (unsigned long long)(k1 - k0));
+  }
   if (nopen != OPEN_WALK) {
     // only the intra members that were open at the first pass can add colours
-    for (u32 k = lane; k < nopen; k += 32) {
-      const i32 u = (i32)__ldcg(rec + CF_HDR + nw + k);
-      const i32 x = wait_final(a, u);
-      const i32 c = -x - 2;
-      if (c >= 1 && c <= CF_WORDS * 32) atomicOr(bm + ((c - 1) >> 5), 1u << ((c - 1) & 31));
+    for (u32 k = lane; k < nopen; k += 32 * 8) {
+      i32 us[8], xs[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) us[q] = k + 32 * q < nopen ? (i32)__ldcg(rec + CF_HDR + nw + k + 32 * q) : -1;
+#pragma unroll
+      for (int q = 0; q < 8; q++) xs[q] = us[q] >= 0 ? ld_relaxed(a.val + us[q]) : 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        if (us[q] < 0) continue;
+        const i32 x = xs[q] == PENDING ? wait_final(a, us[q]) : xs[q];
+        const i32 c = -x - 2;
+        if (c >= 1 && c <= CF_WORDS * 32) atomicOr(bm + ((c - 1) >> 5), 1u << ((c - 1) & 31));
+      }
     }
     __syncwarp();
     const i32 t = warp_mex(bm, lane);
@@ -360,14 +390,14 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
   __shared__ u32 cbm[CF_WORDS];
   __shared__ int cred[3][CF_WARPS];
   __shared__ i32 wlist[CF_WARPS][CF_OPEN];  // open intra members of a long row (first pass)
-  __shared__ i32 clist[CF_OPEN];
+  __shared__ i32 clist[CF_HUB_OPEN];
   __shared__ int wlen[CF_WARPS], clen, glen[CF_WARPS * 4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u32* bm = wbm[wid];
   const i64 gw = (i64)blockIdx.x * CF_WARPS + wid, nwarps = (i64)gridDim.x * CF_WARPS;
   unsigned ntr = 0;
   auto tr = [&](unsigned phase, unsigned count) {
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && ntr < 4094) {
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && ntr < 4090) {
       a.trace[2 + 2 * ntr] = gtimer();
       a.trace[3 + 2 * ntr] = ((unsigned long long)phase << 32) | count;
       a.trace[0] = ++ntr;
@@ -406,6 +436,11 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
       if (v >= 0 && deg > CF_HEAVY) {  // a hub: one accumulator slot, one item per slice
         const int nsl = (int)((deg + CF_SLICE - 1) / CF_SLICE);
         const unsigned slot = atomicAdd(a.hub_top, 1u);
+        if (slot >= a.hub_cap) {  // cannot happen with an exact count; never leave a waiter hanging
+          atomicOr(a.cnt + 6, 1u);
+          publish(a, v, 1);
+          continue;
+        }
         const unsigned base = atomicAdd(bc + 1, (unsigned)nsl);
         u32* hb = a.hub_bm + (i64)slot * CF_WORDS;
         for (int w = 0; w < CF_WORDS; w++) hb[w] = 0;
@@ -437,7 +472,7 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
         if (threadIdx.x == 0) clen = 0;
         __syncthreads();
         RowScan r;
-        first_scan(a, vh, s0, threadIdx.x, CF_THREADS, true, cbm, r, clist, &clen, b0, b1);
+        first_scan(a, vh, s0, threadIdx.x, CF_THREADS, true, cbm, r, clist, &clen, b0, b1, FULLM, a.hub_list);
         r.intra = __reduce_add_sync(FULLM, r.intra);
         r.nlt0 = __reduce_add_sync(FULLM, r.nlt0);
         r.nltv = __reduce_add_sync(FULLM, r.nltv);
@@ -449,23 +484,23 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
         __syncthreads();
         u32* hb = a.hub_bm + (i64)it.x * CF_WORDS;
         int* hc = a.hub_cnt + (i64)it.x * 8;
-        i32* ho = a.hub_open + (i64)it.x * CF_OPEN;
+        i32* ho = a.hub_open + (i64)it.x * CF_HUB_OPEN;
         if (wid == 0) {
           RowScan t{cred[0][lane], cred[1][lane], cred[2][lane]};
           t.intra = __reduce_add_sync(FULLM, t.intra);
           t.nlt0 = __reduce_add_sync(FULLM, t.nlt0);
           t.nltv = __reduce_add_sync(FULLM, t.nltv);
           if (cbm[lane]) atomicOr(hb + lane, cbm[lane]);
-          const int nl = clen < CF_OPEN ? clen : CF_OPEN;
+          const int nl = clen < a.hub_list ? clen : a.hub_list;
           int base = 0;
           if (lane == 0) {
             atomicAdd(hc + 0, t.intra);
             atomicAdd(hc + 1, t.nlt0);
             atomicAdd(hc + 2, t.nltv);
-            base = atomicAdd(hc + 4, clen);  // > CF_OPEN in total: the resolver walks the segment
+            base = atomicAdd(hc + 4, clen);  // > CF_HUB_OPEN in total: the resolver walks the segment
           }
           base = __shfl_sync(FULLM, base, 0);
-          for (int k = lane; k < nl && base + k < CF_OPEN; k += 32) ho[base + k] = clist[k];
+          for (int k = lane; k < nl && base + k < a.hub_list; k += 32) ho[base + k] = clist[k];
           __threadfence();
           __syncwarp();
           if (lane == 0) last = atomicSub(hc + 3, 1) == 1;
@@ -475,10 +510,10 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
           __threadfence();
           cbm[lane] = __ldcg(hb + lane);
           const int nopen = __ldcg(hc + 4);
-          for (int k = lane; k < CF_OPEN && k < nopen; k += 32) clist[k] = __ldcg(ho + k);
+          for (int k = lane; k < a.hub_list && k < nopen; k += 32) clist[k] = __ldcg(ho + k);
           __syncwarp();
           const RowScan t{__ldcg(hc + 0), __ldcg(hc + 1), __ldcg(hc + 2)};
-          first_finish<32>(a, vh, t, cbm, lane, FULLM, 0, clist, nopen);
+          first_finish<32>(a, vh, t, cbm, lane, FULLM, 0, clist, nopen, a.hub_list);
         }
         __syncthreads();
       }
@@ -566,6 +601,16 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
   }
 }
 
+__global__ void k_count_hubs(const i32* wl, i64 n, const i64* rowptr, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i32 v = wl[i];
+    c += rowptr[v + 1] - rowptr[v] > CF_HEAVY;
+  }
+  c = __reduce_add_sync(FULLM, (unsigned)c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 __global__ void k_decode(const i32* wl, i64 n, i32* val) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     const i32 v = wl[i];
@@ -597,18 +642,40 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   const i64 nchunks = nchunks_env > 0 ? nchunks_env : 32;
   i64 chunk = std::max<i64>((i64)1 << 15, (nwl + nchunks - 1) / nchunks);
   if (chunk > nwl) chunk = nwl;
-  // hub rows (deg > CF_HEAVY, so at most nnz / CF_HEAVY of them): one accumulator slot
-  // each; their slices (<= deg / CF_SLICE + 1 per hub) are the chunk's CTA items
+  // hub rows (deg > CF_HEAVY) of the worklist, counted (cached for an iota worklist):
+  // one accumulator slot and open list each; their slices (<= deg / CF_SLICE + 1 per
+  // hub) are the chunk's CTA items
   i64 nnz_all = 0;
   CUDA_CHECK(cudaMemcpyAsync(&nnz_all, L.rowptr + nv, sizeof(i64), cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  const i64 hub_cap = nnz_all / CF_HEAVY + 2;
+  const bool iota = L.wl == nullptr;
+  i64 hubs = 0;
+  if (iota && S.hub_key == L.rowptr && S.hub_key_nv == nv && S.hub_key_base == L.wl_base && S.hub_key_n == nwl) {
+    hubs = S.hub_rows;
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  } else {
+    S.nhubs.reserve(1, s);
+    S.nhubs.zero(s);
+    k_count_hubs<<<grid_for(nwl, 256, num_sms() * 8), 256, 0, s>>>(wl, nwl, L.rowptr, S.nhubs.p);
+    count_launch();
+    unsigned long long h = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&h, S.nhubs.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    hubs = (i64)h;
+    if (iota) {
+      S.hub_key = L.rowptr;
+      S.hub_key_nv = nv;
+      S.hub_key_base = L.wl_base;
+      S.hub_key_n = nwl;
+      S.hub_rows = hubs;
+    }
+  }
+  const i64 hub_cap = hubs + 1;
   const i64 item_cap = chunk + nnz_all / CF_SLICE + 2;
   S.heavy.reserve(2 * chunk + item_cap, s);
   S.slice.reserve(item_cap, s);
   S.hub_bm.reserve(hub_cap * CF_WORDS, s);
   S.hub_cnt.reserve(hub_cap * 8, s);
-  S.hub_open.reserve(hub_cap * CF_OPEN, s);
+  S.hub_open.reserve(hub_cap * CF_HUB_OPEN, s);
   S.hub_top.reserve(1, s);
   CUDA_CHECK(cudaMemsetAsync(S.hub_top.p, 0, sizeof(unsigned), s));
   S.cnt.reserve(8, s);
@@ -616,7 +683,8 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   S.desc.reserve(nv, s);
   const i64 nnz = nnz_all;
   // bitmaps (<= deg/32 + 2 words), headers, and open lids (<= intra entries <= nnz)
-  const i64 pool_words = nnz / 32 + (i64)(CF_HDR + 4) * nwl + std::min<i64>(nnz, (i64)CF_OPEN * nwl) + 4096;
+  const i64 pool_words = nnz / 32 + (i64)(CF_HDR + 4) * nwl +
+                         std::min<i64>(nnz, (i64)CF_OPEN * nwl + (i64)CF_HUB_OPEN * hubs) + 4096;
   S.pool.reserve(pool_words, s);
   S.pool_top.reserve(1, s);
   S.pool_top.zero(s);
@@ -638,6 +706,14 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   a.hub_cnt = S.hub_cnt.p;
   a.hub_open = S.hub_open.p;
   a.hub_top = S.hub_top.p;
+  a.hub_cap = (unsigned)hub_cap;
+  // measured (C3): long hub lists pay in later rounds (dense cores of recoloured hubs,
+  // whose segments are long) and cost in round 0 (rows read up to the vertex only)
+  static const int hub_list_env = [] {
+    const char* e = std::getenv("CHROMA_GS_HUB_OPEN");
+    return e ? std::max(1, std::min(CF_HUB_OPEN, std::atoi(e))) : 0;
+  }();
+  a.hub_list = hub_list_env ? hub_list_env : a.upper_zero ? CF_OPEN : CF_HUB_OPEN;
   a.cnt = S.cnt.p;
   a.pool = S.pool.p;
   a.pool_top = S.pool_top.p;
@@ -672,8 +748,11 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
       ph_t[(unsigned)(h[3 + 2 * i] >> 32) & 3] += h[2 + 2 * i] - tp;
       tp = h[2 + 2 * i];
     }
-    std::fprintf(stderr, "[gs_chunked] nwl %lld chunk %lld: short rows %.1f us, long rows %.1f us, dataflow %.1f us\n",
-                 (long long)nwl, (long long)chunk, ph_t[1] * 1e-3, ph_t[2] * 1e-3, ph_t[3] * 1e-3);
+    std::fprintf(stderr,
+                 "[gs_chunked] nwl %lld chunk %lld: short rows %.1f us, long rows %.1f us, dataflow %.1f us; "
+                 "lane walks %llu (%llu entries), open hubs %llu (walked %llu entries)\n",
+                 (long long)nwl, (long long)chunk, ph_t[1] * 1e-3, ph_t[2] * 1e-3, ph_t[3] * 1e-3, h[8190], h[8191],
+                 h[8188], h[8189]);
   }
   unsigned ovf = 0;
   CUDA_CHECK(cudaMemcpyAsync(&ovf, S.cnt.p + 6, sizeof(unsigned), cudaMemcpyDeviceToHost, s));

@@ -14,6 +14,6 @@ for P in Ps:
             c, reps = R.run_distributed(w, cfg)
         tc = sum(r.time_color_s for r in reps) * 1e3; tm = sum(r.time_comm_s for r in reps) * 1e3; td = sum(r.time_detect_s for r in reps) * 1e3
         print(f"P={P} {algo}: rounds {len(reps)} color {tc:.1f} comm {tm:.1f} detect {td:.1f} ms; bytes {sum(r.bytes_sent for r in reps)}", flush=True)
-        for r in reps[:4]:
+        for r in reps:
             print(f"   r{r.round_index}: conflicts {r.conflicts} recol {sum(r.recolored_per_rank)} color {r.time_color_s*1e3:.2f} comm {r.time_comm_s*1e3:.2f} detect {r.time_detect_s*1e3:.2f}", flush=True)
     del w
