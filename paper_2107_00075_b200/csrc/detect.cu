@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(1024, 1) k_resolve_grid(const int2* ev, i64 E,
 // vertices finds every scanned pair (v ghost, x in row(v)) with equal colours:
 // from changed y, (y, x) when y is a ghost, (x, y) when x is.  Keys (v << 32 | x)
 // sorted and de-duplicated are exactly the reference's scan order (ghost rows
-// ascending, each row ascending).  WRITE = false counts.
+// ascending, each row ascending).  WRITE = false counts; with WRITE, keys beyond cap
+// are counted but not stored (the caller grows the buffer and emits again).
 constexpr i64 SEG = 256;  // row entries per work item of the changed-side walk
 
 // segments of the long (> 32 entries) source rows; short ones go to k_emit_short
@@ -303,7 +304,7 @@ __global__ void k_changed_nseg(const i64* rowptr, const i32* changed, i64 nch, i
 // changed vertices, emit (y, x) if y is a ghost and (x, y) if x is.
 template <bool WRITE, bool ROWS>
 __global__ void k_emit_short(const i64* rowptr, const i32* col, const i32* colors, const uint8_t* owned,
-                             const i32* src, i64 nsrc, unsigned long long* cnt, u64* keys) {
+                             const i32* src, i64 nsrc, unsigned long long* cnt, u64* keys, unsigned long long cap) {
   const int lane = threadIdx.x & 31;
   for (i64 b = (blockIdx.x * (i64)blockDim.x + threadIdx.x) - lane; b < nsrc; b += (i64)gridDim.x * blockDim.x) {
     const i64 i = b + lane;
@@ -350,8 +351,10 @@ __global__ void k_emit_short(const i64* rowptr, const i32* col, const i32* color
           if (pass == 0) {
             k += (gy ? 1u : 0u) + (gs[q] ? 1u : 0u);
           } else {
-            if (gy) keys[at++] = ((u64)(u32)y << 32) | (u32)xs[q];
-            if (gs[q]) keys[at++] = ((u64)(u32)xs[q] << 32) | (u32)y;
+            if (gy && at < cap) keys[at] = ((u64)(u32)y << 32) | (u32)xs[q];
+            at += gy;
+            if (gs[q] && at < cap) keys[at] = ((u64)(u32)xs[q] << 32) | (u32)y;
+            at += gs[q];
           }
         }
       }
@@ -369,7 +372,7 @@ __global__ void k_emit_short(const i64* rowptr, const i32* col, const i32* color
 template <bool WRITE, bool ROWS>
 __global__ void k_changed_events(const i64* rowptr, const i32* col, const i32* colors, const uint8_t* owned,
                                  const i32* changed, i64 nch, const i64* segoff, i64 nitems,
-                                 unsigned long long* cnt, u64* keys) {
+                                 unsigned long long* cnt, u64* keys, unsigned long long cap) {
   const int lane = threadIdx.x & 31;
   const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
@@ -422,8 +425,9 @@ __global__ void k_changed_events(const i64* rowptr, const i32* col, const i32* c
       }
       if (k) {
         unsigned long long at = base + inc - k;
-        if (gy) keys[at++] = ((u64)(u32)y << 32) | (u32)x;
-        if (gx) keys[at] = ((u64)(u32)x << 32) | (u32)y;
+        if (gy && at < cap) keys[at] = ((u64)(u32)y << 32) | (u32)x;
+        at += gy;
+        if (gx && at < cap) keys[at] = ((u64)(u32)x << 32) | (u32)y;
       }
     }
     if (!WRITE) {
@@ -760,30 +764,36 @@ static i64 keyed_events(const DetectArgs& A, const DevDetect& a, DetectScratch& 
   CUDA_CHECK(cudaStreamSynchronize(s));
   const int gs = grid_for(nsrc, 256, num_sms() * 16);
   const int gw = grid_for(std::max<i64>(nitems, 1) * 32, 256, num_sms() * 16);
-  auto emit = [&](auto write, u64* keys) {
-    constexpr bool W = decltype(write)::value;
+  // one emission pass into a buffer sized by the previous call; a second, exact one
+  // only when that was too small
+  auto emit = [&](u64* keys, unsigned long long cap) {
     if (rows_mode) {
-      k_emit_short<W, true><<<gs, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.nch.p, keys);
+      k_emit_short<true, true><<<gs, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.nch.p, keys,
+                                                  cap);
       if (nitems)
-        k_changed_events<W, true><<<gw, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.off.p,
-                                                     nitems, S.nch.p, keys);
+        k_changed_events<true, true><<<gw, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.off.p,
+                                                        nitems, S.nch.p, keys, cap);
       count_launch(nitems ? 2 : 1);
     } else {
       if (nitems)
-        k_changed_events<W, false><<<gw, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.off.p,
-                                                      nitems, S.nch.p, keys);
+        k_changed_events<true, false><<<gw, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc,
+                                                         S.off.p, nitems, S.nch.p, keys, cap);
       count_launch();
     }
   };
-  emit(std::false_type{}, nullptr);
+  i64 cap = std::max<i64>(S.keys.n, (i64)1 << 20);
+  S.keys.reserve(cap, s);
+  emit(S.keys.p, (unsigned long long)cap);
   unsigned long long nku = 0;
   CUDA_CHECK(cudaMemcpyAsync(&nku, S.nch.p, sizeof(nku), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
   const i64 nk = (i64)nku;
   if (nk == 0) return 0;
-  S.keys.reserve(nk, s);
-  CUDA_CHECK(cudaMemsetAsync(S.nch.p, 0, sizeof(unsigned long long), s));
-  emit(std::true_type{}, S.keys.p);
+  if (nk > cap) {
+    S.keys.reserve(nk, s);
+    CUDA_CHECK(cudaMemsetAsync(S.nch.p, 0, sizeof(unsigned long long), s));
+    emit(S.keys.p, (unsigned long long)nk);
+  }
   sort_u64(S.keys.p, nk, s);
   S.ukeys.reserve(nk, s);
   const i64 E = unique_u64(S.keys.p, nk, S.ukeys.p, s);
