@@ -500,15 +500,16 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   w.det.prev_valid = false;
   const bool remote = w.connected && w.P > 1;
   bool hubs_done = false;
-  // CHROMA_ROUND_TRACE: synchronised per-phase host timings of round 0 (dev aid)
+  // CHROMA_ROUND_TRACE[=r]: synchronised per-phase host timings of round r (default 0; dev aid)
   static const bool round_trace = std::getenv("CHROMA_ROUND_TRACE") != nullptr;
+  static const i64 trace_round = env_i64("CHROMA_ROUND_TRACE", 0);
   auto rt_last = std::chrono::steady_clock::now();
   i64 rt_round = 0;
   auto rt_mark = [&](const char* what) {
-    if (!round_trace || rt_round != 0) return;
+    if (!round_trace || rt_round != trace_round) return;
     CUDA_CHECK(cudaStreamSynchronize(s));
     const auto tn = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[round0] %-18s %8.1f us\n", what, std::chrono::duration<double, std::micro>(tn - rt_last).count());
+    std::fprintf(stderr, "[round%lld] %-18s %8.1f us\n", (long long)rt_round, what, std::chrono::duration<double, std::micro>(tn - rt_last).count());
     rt_last = tn;
   };
   for (;;) {

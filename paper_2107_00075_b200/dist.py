@@ -133,11 +133,22 @@ class DistWorld:
             raise ValueError("one process per rank is required")
         self.device = torch.cuda.current_device() if device is None else device
         _lib.set_device(self.device)
+        import os
+        import time
+        timing = os.environ.get("CHROMA_BUILD_TIMING") is not None
+        t_last = [time.perf_counter()]
+
+        def mark(what):  # CHROMA_BUILD_TIMING: host-side phase times of this constructor
+            if timing:
+                t = time.perf_counter()
+                print(f"[distworld r{self.rank}] {what:<10} {1e3 * (t - t_last[0]):8.2f} ms", flush=True)
+                t_last[0] = t
         self.ghost_layers = ghost_layers
         self.partition = pm
         self.num_global_vertices = g.num_vertices
         # owner validation happens in the device builder (chroma_world_create)
         self.handle = WorldHandle(g, pm, ghost_layers, self.rank, self.rank + 1, self.device)
+        mark("handle")
         self.source_stats = device_stats(self.handle)
         self.local_graph = LocalGraph(self.handle, self.rank, ghost_layers)
         self.local_graphs = [self.local_graph]
@@ -159,11 +170,14 @@ class DistWorld:
             if len(_ROUTES) >= 4:
                 _ROUTES.pop(next(iter(_ROUTES)))
             _ROUTES[key] = (g.row_offsets, g.col_indices, pm.owner, routing)
+        mark("routing")
         self.comm = communicator(group, self.num_ranks, self.rank, self.device)
         sc, sl, rc, rl = (_lib.i64(x) for x in routing)
+        mark("comm")
         _lib.check(_lib.lib().chroma_world_connect(self.handle.h, self.comm.h, self.num_ranks, self.rank,
                                                    _lib.ptr(sc), _lib.ptr(sl), _lib.ptr(rc), _lib.ptr(rl)),
                    "chroma_world_connect")
+        mark("connect")
         self.halo_send = int(sc.sum())
         self.halo_recv = int(rc.sum())
 
