@@ -57,6 +57,28 @@ void launch_jacobi_losers(const i64* rowptr, const i32* col, i32* colors, const 
 
 // Edge-based Jacobi sweep (Kernel.EDGE_BASED, distance 1): proposals into prop, the
 // commit, and losers into lose, edge-parallel over the pending rows.
+// incremental Jacobi state (jacobi_inc.cu)
+struct JacobiIncScratch {
+  DBuf<uint8_t> pendf, hlose;
+  DBuf<i32> hslot, hv, llen, nb, hprop;
+  DBuf<i32> act[4];  // active slots: [2 * class + parity], class 0 warp, 1 CTA
+  DBuf<u32> fb;
+  DBuf<i64> loff, len64;
+  DBuf<unsigned long long> cnt;  // [0] heavy slots, [1] overflow, [2 + 2 * class + parity] active counts
+  i64 nheavy = 0;
+  int par = 0;
+  bool on = false;
+};
+bool jacobi_inc_init(const i64* rowptr, const i32* col, const i32* colors, const i32* pend, i64 np, i64 nv,
+                     JacobiIncScratch& S, cudaStream_t s);
+void jacobi_inc_propose(const i64* rowptr, const i32* col, const i32* colors, const i32* pend, const i64* np_dev,
+                        i64 np, i32* prop, JacobiIncScratch& S, cudaStream_t s);
+void jacobi_inc_losers(const i64* rowptr, const i32* col, const i32* colors, const i32* pend, const i64* np_dev,
+                       i64 np, const uint8_t* in_round, uint8_t* lose, JacobiIncScratch& S, cudaStream_t s);
+void jacobi_inc_update(const i32* colors, const i32* pend, const i64* np_dev, i64 np, const uint8_t* lose,
+                       JacobiIncScratch& S, cudaStream_t s);
+const unsigned* jacobi_inc_overflow_dev(const JacobiIncScratch& S);
+
 struct EbScratch {
   DBuf<i64> len, eoff, np;
   DBuf<u32> mask;

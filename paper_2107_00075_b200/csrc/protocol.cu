@@ -312,9 +312,26 @@ gauss_seidel:
   CUDA_CHECK(cudaMemcpyAsync(S.np2.p, nwl, sizeof(i64), cudaMemcpyDeviceToDevice, s));
   i32* pend = S.val.p;
   i64 np = read_i64(nwl, s);  // exact count: the compaction below takes a host length
+  // after sweep 0, long pending rows are kept incrementally (jacobi_inc.cu): same
+  // proposals and losers, rows not re-read every sweep
+  static const bool no_inc = std::getenv("CHROMA_JACOBI_FULL") != nullptr;
+  S.ji.on = false;
+  static const bool jtrace = std::getenv("CHROMA_JACOBI_TRACE") != nullptr;
   for (int sweep = 0; sweep < MAX_SWEEPS; sweep++) {
+    if (jtrace && (sweep < 8 || (sweep & (sweep - 1)) == 0 || np == 0)) {
+      static auto jt = std::chrono::steady_clock::now();
+      const auto tn = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[jacobi] sweep %d pending %lld%s (+%.0f us)\n", sweep, (long long)np,
+                   S.ji.on ? " inc" : "", std::chrono::duration<double, std::micro>(tn - jt).count());
+      jt = tn;
+    }
     if (np == 0) return;
-    if (edge_based && dist == 1) {
+    if (S.ji.on) {
+      jacobi_inc_propose(rowptr, col, colors, pend, S.np2.p, np, S.prop.p, S.ji, s);
+      launch_scatter_idx_values(colors, pend, S.prop.p, S.np2.p, np, s);
+      jacobi_inc_losers(rowptr, col, colors, pend, S.np2.p, np, S.in_round.p, S.flags.p, S.ji, s);
+      jacobi_inc_update(colors, pend, S.np2.p, np, S.flags.p, S.ji, s);
+    } else if (edge_based && dist == 1) {
       launch_jacobi_eb(rowptr, col, colors, pend, np, S.prop.p, S.in_round.p, S.flags.p, S.eb, s);
     } else {
       launch_jacobi_propose(rowptr, col, colors, pend, S.np2.p, np, S.prop.p, dist, partial, s);
@@ -322,10 +339,16 @@ gauss_seidel:
                            dist, partial, s);
     }
     select_flagged_values(pend, S.flags.p, np, S.pend2.p, S.np2.p, s);
-    np = read_i64(S.np2.p, s);
+    unsigned ovf = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&np, S.np2.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
+    if (S.ji.on) CUDA_CHECK(cudaMemcpyAsync(&ovf, jacobi_inc_overflow_dev(S.ji), sizeof(ovf), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
     launch_scatter_const(colors, S.pend2.p, S.np2.p, np, 0, s);
     std::swap(S.pend2, S.val);
     pend = S.val.p;
+    if (ovf) S.ji.on = false;  // a colour fb cannot hold: full sweeps from here
+    if (sweep == 0 && dist == 1 && np > 0 && !no_inc)
+      jacobi_inc_init(rowptr, col, colors, pend, np, nv, S.ji, s);
   }
   // the reference raises after the last sweep even if it settled (chroma/localcolor.py:218-227)
   throw Error(CHROMA_ERUNTIME, "speculative loop failed to settle");

@@ -60,6 +60,7 @@ struct ColorScratch {
   ChunkedScratch chunked;
   NetScratch net;
   EbScratch eb;
+  JacobiIncScratch ji;
   bool upper_zero = false;  // gs_chunked: no neighbour above a member is coloured yet
 };
 
