@@ -132,8 +132,11 @@ int chroma_csr_create(int64_t n, const int64_t* off, const int64_t* col, int dev
       narrow_ids_checked(col, nnz, n, dev(flags), h->g.col.p, s, "col_indices out of range");
       CUDA_CHECK(cudaStreamSynchronize(s));
     } catch (...) {
-      if (h->g.stream) cudaStreamDestroy(h->g.stream);
+      // the buffers free on the stream: release them before the stream goes
+      cudaStream_t st = h->g.stream;
+      if (st) cudaStreamSynchronize(st);
       delete h;
+      if (st) cudaStreamDestroy(st);
       throw;
     }
     *out = h;

@@ -47,9 +47,14 @@ def graph(key):
 
 
 def run(g, mode, P, algorithm=None):
+    """algorithm None: deterministic (Gauss-Seidel); "jacobi": the reference's default
+    speculative sweeps; "free": the free-running extension."""
     pm = PT.partition_block(g, P)
     w = RT.build_local_graphs(g, pm, R.ghost_layers_for(R.Mode(mode)))
-    cfg = R.AlgorithmConfig(mode=R.Mode(mode), deterministic=algorithm is None, algorithm=algorithm)
+    if algorithm == "jacobi":
+        cfg = R.AlgorithmConfig(mode=R.Mode(mode))
+    else:
+        cfg = R.AlgorithmConfig(mode=R.Mode(mode), deterministic=algorithm is None, algorithm=algorithm)
     colors, reports = R.run_distributed(w, cfg)
     del w
     return np.asarray(colors), reports
@@ -77,12 +82,14 @@ def test_device_generator_matches_oracle_generator(key):
 
 @pytest.mark.parametrize("key,run_key", DET, ids=[f"{k}-{r}" for k, r in DET])
 def test_deterministic_bit_exact(key, run_key):
+    # keys: <mode>_p<P> (Gauss-Seidel) or <mode>_p<P>_jacobi (default Jacobi sweeps)
     mode, P = run_key.rsplit("_p", 1)
+    P, _, alg = P.partition("_")
     ref = SCALE[key][run_key]
     if mode == "pd2" and key == "c5_2p22":
         pytest.skip("deterministic PD2 at 2^22 is checked at 2^20 (c5_2p20); 2^22 runs free-mode below")
     g = graph(key)
-    colors, reports = run(g, mode, int(P))
+    colors, reports = run(g, mode, int(P), algorithm=alg or None)
     assert sha(colors) == ref["sha256"]
     assert len(reports) == ref["rounds"]
     assert [r.conflicts for r in reports] == ref["conflicts"]
@@ -133,3 +140,21 @@ def test_host_arrays_serial_greedy_and_range_check():
         RT.build_local_graphs(bg, PT.partition_block(bg, 1), 1)
     with pytest.raises(ValueError, match="out of range"):
         L.serial_greedy(bg)
+
+
+@pytest.mark.parametrize("P,threshold", [(1, 6000), (1, 1), (3, 6000), (3, 1)])
+def test_jacobi_incremental_matches_oracle(P, threshold):
+    # the reference's default mode: sweep 0 by VB or EB (threshold), incremental
+    # sweeps after it (csrc/jacobi_inc.cu); colours and per-round counts bit-exact
+    import oracle
+    from paper_2107_00075_b200 import localcolor as L
+    g = G.gen_rmat(16, 16, 5, device="cuda")
+    pm = PT.partition_block(g, P)
+    w = RT.build_local_graphs(g, pm, 1)
+    cfg = R.AlgorithmConfig(mode=R.Mode.D1, kernel=L.KernelChoice(max_degree_threshold=threshold))
+    colors, reports = R.run_distributed(w, cfg)
+    ow = oracle.World(np.asarray(g.row_offsets), np.asarray(g.col_indices), pm.owner, P, 1)
+    rc, rr = ow.run("d1", False, False)
+    assert np.array_equal(np.asarray(colors), rc)
+    assert [r.conflicts for r in reports] == [r["conflicts"] for r in rr]
+    assert [list(r.recolored_per_rank) for r in reports] == [r["recolored_per_rank"] for r in rr]
