@@ -70,7 +70,7 @@ ITEMS = {
     "c1_1000": (lambda: hex_mesh(1000, 1000, 1), [(1, "d1", 1)]),
     # name: (graph builder, [(P, mode, ghost layers[, "jacobi"])]); "jacobi": the
     # reference's default speculative mode (deterministic=False), key suffix _jacobi
-    "c3_s24": (lambda: oracle.gen_rmat(24), [(1, "d1", 1), (8, "d1", 1), (1, "d1", 1, "jacobi")]),
+    "c3_s24": (lambda: oracle.gen_rmat(24), [(1, "d1", 1), (8, "d1", 1), (1, "d1", 1, "jacobi"), (4, "d1", 1, "jacobi")]),
     "c5_2p20": (lambda: oracle.gen_bipartite(1 << 20, 32, 3), [(1, "pd2", 2), (8, "pd2", 2)]),
     "c4_200": (lambda: hex_mesh(200, 200, 200), [(8, "d2", 2), (1, "d2", 2)]),
     "c2_128": (lambda: stencil27(128), [(2, "d1-2gl", 2), (4, "d1-2gl", 2), (8, "d1-2gl", 2)]),
