@@ -8,7 +8,8 @@ per GPU), deterministic mode -- the reference's Gauss-Seidel semantics, bit-exac
 the C oracle (the colour array's sha256 is printed beside the oracle's).  One step =
 one full run_distributed on the device-resident world, colours left in HBM; nothing is
 cached between steps (the chunked Gauss-Seidel kernel builds everything it needs per
-call).  A "free" sub-record times the free-running mode on the same world.
+call).  A "free" sub-record times the free-running mode on the same world, and a "jacobi"
+sub-record the reference's default mode (Jacobi sweeps) with its sha against the oracle's.
 
     python bench.py [--gpus N --steps K --warmup W]            # our B200 path (C3)
     python bench.py --workload c1|c2|c4|c5 [...]                # other BASELINE configs
@@ -431,6 +432,22 @@ def main():
                     "colors": fn, "oracle_deterministic_colors": ref_n,
                     "within_5pct": (fn <= 1.05 * ref_n) if ref_n else None,
                     "violations": V.count_violations(g, fcol, wl.vmode)}
+    # ---- the reference's default mode (Jacobi sweeps, deterministic=False) on the same world
+    jac = None
+    if not args.no_free and cfg.deterministic and wl.name == "c3":
+        jcfg = R.AlgorithmConfig(mode=R.Mode(wl.mode))  # the reference's defaults
+        jsteps = max(1, min(args.steps, 2))
+        jper, _, jreps, _ = timed_steps(jcfg, jsteps, 1)
+        Tj = allmax(sum(jper))
+        jcol = gather_colors()
+        if rank == 0:
+            jsha = sha256_i32(jcol)
+            jref = (gold or {}).get(f"{wl.mode}_p{N}_jacobi") or {}
+            jac = {"value": m * jsteps / Tj, "ms_per_step": 1e3 * Tj / jsteps, "rounds": len(jreps),
+                   "colors": V.color_stats(jcol)[0], "colour_sha256": jsha,
+                   "oracle_sha256": jref.get("sha256"),
+                   "match": (jref.get("sha256") == jsha) if jref.get("sha256") else None,
+                   "oracle_run_s": jref.get("oracle_run_s")}
     # ---- roofline of the dominant kernel (the round-0 colouring)
     n_o = lg.owned_count
     nnz_o = int(lg.row_offsets[n_o]) if N > 1 else len(g.col_indices)
@@ -465,10 +482,15 @@ def main():
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 wv = make_world(graph, partition)
+                t1 = time.perf_counter()
                 colors, _ = R.run_distributed(wv, cfg)
                 torch.cuda.synchronize()
                 el = time.perf_counter() - t0
+                t2 = time.perf_counter()
                 del wv, colors
+                if os.environ.get("CHROMA_E2E_TRACE"):
+                    print(f"[e2e] step {it}: build {1e3 * (t1 - t0):.1f} ms, run {1e3 * (el - (t1 - t0)):.1f} ms, "
+                          f"release {1e3 * (time.perf_counter() - t2):.1f} ms", file=sys.stderr, flush=True)
                 if it >= W:
                     et.append(el)
             return allmax(sum(et) / len(et))
@@ -501,7 +523,7 @@ def main():
                                       if wl.name == "c3" else "per-world round-0 schedule built in warm-up",
                            "cold_call_ms": cold_ms,
                            "l2": f"inputs larger than L2 (int32 col {4 * len(g.col_indices) / 1e6:.0f} MB)"},
-                "parity": parity, "free": free,
+                "parity": parity, "free": free, "jacobi": jac,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak if achieved else None, "traffic": traffic,
                              "kernel": kname, "algorithmic_bytes_per_launch": B, "kernel_ms": kernel_s * 1e3,

@@ -647,9 +647,12 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   // hub) are the chunk's CTA items
   i64 nnz_all = 0;
   CUDA_CHECK(cudaMemcpyAsync(&nnz_all, L.rowptr + nv, sizeof(i64), cudaMemcpyDeviceToHost, s));
-  const bool iota = L.wl == nullptr;
+  // cacheable: an iota worklist, or the round-0 worklist of a world (every owned
+  // vertex: the same set on every call of this scratch's world)
+  const bool iota = L.wl == nullptr || upper_zero;
   i64 hubs = 0;
-  if (iota && S.hub_key == L.rowptr && S.hub_key_nv == nv && S.hub_key_base == L.wl_base && S.hub_key_n == nwl) {
+  if (iota && S.hub_key == L.rowptr && S.hub_key_nv == nv && S.hub_key_base == L.wl_base && S.hub_key_n == nwl &&
+      S.hub_key_wl == L.wl) {
     hubs = S.hub_rows;
     CUDA_CHECK(cudaStreamSynchronize(s));
   } else {
@@ -666,6 +669,7 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
       S.hub_key_nv = nv;
       S.hub_key_base = L.wl_base;
       S.hub_key_n = nwl;
+      S.hub_key_wl = L.wl;
       S.hub_rows = hubs;
     }
   }

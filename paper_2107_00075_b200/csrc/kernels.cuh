@@ -40,6 +40,7 @@ struct ChunkedScratch {
   DBuf<unsigned long long> nhubs;
   // hub-row count of the last iota worklist (round 0 of a world): key and value
   const i64* hub_key = nullptr;
+  const i32* hub_key_wl = nullptr;
   i64 hub_key_nv = -1, hub_key_base = -1, hub_key_n = -1, hub_rows = 0;
 };
 // upper_zero: every neighbour above a worklist member contributes colour 0 (round 0:

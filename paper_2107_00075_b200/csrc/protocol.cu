@@ -571,7 +571,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
       select_flagged(w.cs.flags.p, w.NL, w.cs.wl.p, w.cs.nwl.p, s);
       nwl_host = w.NL;
     }
-    k_count_recolored<<<std::min(G(w.NL), num_sms() * 2), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
+    k_count_recolored<<<grid_for(w.NL, 256, num_sms() * 16), 256, 0, s>>>(w.cs.wl.p, w.cs.nwl.p, w.owned_flag.p, w.rank_of.p, w.rank_lo,
                                               w.rank_hi - w.rank_lo, w.stats.p);
     count_launch();
     const bool gs_like = !is_jacobi;
