@@ -447,6 +447,14 @@ ClusterKernel cluster_kernel(int DW) {
 }  // namespace
 
 // ---------------------------------------------------------------- plan
+// Largest vertex count whose colour bytes fit the cluster's shared memory (16 CTAs).
+i64 cluster_max_vertices() {
+  int dev = 0, max_smem = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  return std::max<i64>(0, (i64)max_smem - 32 * 1024) * 16;
+}
+
 bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
                         i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s,
                         bool chains, bool zero_nm) {

@@ -264,7 +264,10 @@ gauss_seidel:
     }
     static const bool no_chunked = std::getenv("CHROMA_NO_CHUNKED") != nullptr;
     const bool cluster = S.level_wl && S.level_mode && S.cplan && dist == 1 && !L.old;
-    if (dist == 1 && !cluster && !no_chunked) {
+    // a level schedule without the cluster (too many vertices for its shared memory):
+    // the level-ordered dataflow kernel; otherwise the chunked one
+    const bool levels = S.level_wl && S.level_mode && !cluster;
+    if (dist == 1 && !cluster && !levels && !no_chunked) {
       // chunked fixed point over the original worklist (gs_chunked.cu)
       const i64 nexact = wl_sorted_unique && nwl != nullptr ? read_i64(nwl, s) : nwl_max;
       GsLaunch C = L;
@@ -522,6 +525,24 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   da.owned_flag = w.owned_flag.p;
   w.det.prev_valid = false;
   const bool remote = w.connected && w.P > 1;
+  // Distance 2 without the partial (bipartite) restriction, Gauss-Seidel or Jacobi, on
+  // a bounded-degree graph: the distance-1 kernels on the square G^2 (square.cu) --
+  // identical forbidden sets, orders and loser rule.  Detection stays on G.
+  static const bool no_square = std::getenv("CHROMA_NO_SQUARE") != nullptr;
+  bool use_sq = false;
+  if (d2 && !partial && algo != CHROMA_ALGO_FREE && !no_square && w.delta_max <= 11) {
+    if (w.sq_state == 0) {
+      i64 md = 0;
+      w.sq_state = build_square(w.g.rowptr.p, w.g.col.p, w.NL, nullptr, w.sq_rowptr, w.sq_col, md, s) ? 1 : -1;
+      w.sq_delta = md;
+    }
+    use_sq = w.sq_state == 1;
+  }
+  const i64* crow = use_sq ? w.sq_rowptr.p : w.g.rowptr.p;
+  const i32* ccol = use_sq ? w.sq_col.p : w.g.col.p;
+  const int cdist = use_sq ? 1 : dist;
+  const i64 cdelta = use_sq ? w.sq_delta : w.delta_max;
+  if (w.level_n >= 0 && w.level_sq != use_sq) w.level_n = -1;  // a schedule of the other graph
   bool hubs_done = false;
   // CHROMA_ROUND_TRACE[=r]: synchronised per-phase host timings of round r (default 0; dev aid)
   static const bool round_trace = std::getenv("CHROMA_ROUND_TRACE") != nullptr;
@@ -580,8 +601,9 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     // The schedule is built from round 0's full owned worklist and cached per world:
     // not when hubs were pre-coloured (the worklist then lacks them), and only for
     // bounded degree (the cluster kernel); other graphs take gs_chunked.cu.
-    if (round == 0 && dist == 1 && gs_like && !no_levels && !hubs_done && w.delta_max <= 32) {
+    if (round == 0 && cdist == 1 && gs_like && !no_levels && !hubs_done && cdelta <= 32) {
       if (w.level_n < 0) {
+        w.level_sq = use_sq;
         i64 owned = 0;
         std::vector<i64> counts;
         for (auto& m : w.ranks) {
@@ -592,18 +614,18 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
         // levels when the DAG is wide; else (virtual ranks) rank-interleaved id order
         // bounded degree <= 32: try the cluster kernel (gs_cluster.cu), which walks
         // narrow levels as cheaply as wide ones; otherwise only wide DAGs take levels
-        const bool try_cluster = w.delta_max <= 32 && !no_cluster;
+        const bool try_cluster = cdelta <= 32 && !no_cluster && w.NL <= cluster_max_vertices();
         // the cluster kernel resolves runs of adjacent consecutive ids in one level
         const bool chains = try_cluster && !no_chains;
         std::vector<i64> lsizes;
         static const bool ltrace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
         const auto lt0 = std::chrono::steady_clock::now();
-        w.level_mode = (sched == 0 || sched == 1) && w.delta_max <= level_max_deg &&
-                       build_level_order(w.g.rowptr.p, w.g.col.p, w.NL, w.cs.wl.p, owned, w.level_wl, n, s,
+        w.level_mode = (sched == 0 || sched == 1) && cdelta <= level_max_deg &&
+                       build_level_order(crow, ccol, w.NL, w.cs.wl.p, owned, w.level_wl, n, s,
                                          &lsizes, try_cluster ? 1 : -1, chains);
         const auto lt1 = std::chrono::steady_clock::now();
         if (w.level_mode && try_cluster &&
-            !build_cluster_plan(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, w.level_wl.p, n, lsizes, w.cplan, s,
+            !build_cluster_plan(crow, ccol, w.NL, cdelta, w.level_wl.p, n, lsizes, w.cplan, s,
                                 chains, !hubs_done)) {
           // no cluster: keep the schedule only if it is wide enough for the dataflow
           // kernel (and has no runs, which only the cluster kernel evaluates)
@@ -633,7 +655,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     }
     rt_mark("hubs+worklist");
     w.cs.upper_zero = round == 0 && !hubs_done;  // nothing is coloured before round 0
-    color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, nwl_host, true, dist, partial,
+    color_csr(crow, ccol, w.NL, w.colors.p, w.cs.wl.p, w.cs.nwl.p, nwl_host, true, cdist, partial,
               algo, true, w.cs, s, gs_like ? ev[6] : nullptr, gs_like ? ev[7] : nullptr);
     rt_mark("color");
     w.cs.level_wl = nullptr;

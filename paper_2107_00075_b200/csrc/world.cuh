@@ -146,7 +146,14 @@ struct World {
   DBuf<i32> level_wl;
   i64 level_n = -1;
   bool level_mode = false;
+  bool level_sq = false;  // the schedule is of the square (distance-2 runs)
   ClusterPlan cplan;
+  // the square of the local graph (square.cu), built on the first
+  // distance-2 run of a bounded-degree world: 0 not yet, 1 built, -1 not applicable
+  int sq_state = 0;
+  DBuf<i64> sq_rowptr;
+  DBuf<i32> sq_col;
+  i64 sq_delta = 0;
   // device-side timing of the last run_distributed (CUDA events on `stream`)
   double t_total = 0, t_color_kernel = 0, t_color = 0, t_comm = 0, t_detect = 0;
 
@@ -190,6 +197,7 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
 // Level-synchronous Gauss-Seidel on one thread-block cluster (gs_cluster.cu): the
 // plan is built once from a level schedule (bounded degree <= 32, colours of every
 // vertex fit the cluster's shared memory as bytes); false if not applicable.
+i64 cluster_max_vertices();
 bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
                         i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s,
                         bool chains = false, bool zero_nonmembers = false);
