@@ -525,16 +525,22 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   da.owned_flag = w.owned_flag.p;
   w.det.prev_valid = false;
   const bool remote = w.connected && w.P > 1;
-  // Distance 2 without the partial (bipartite) restriction, Gauss-Seidel or Jacobi, on
-  // a bounded-degree graph: the distance-1 kernels on the square G^2 (square.cu) --
-  // identical forbidden sets, orders and loser rule.  Detection stays on G.
+  // Distance 2 without the partial (bipartite) restriction on a bounded-degree graph:
+  // the distance-1 kernels on the square G^2 (square.cu) -- identical forbidden sets,
+  // orders and loser rule (Gauss-Seidel, Jacobi; the free mode colours such graphs by
+  // Gauss-Seidel too).  Detection stays on G.
   static const bool no_square = std::getenv("CHROMA_NO_SQUARE") != nullptr;
   bool use_sq = false;
-  if (d2 && !partial && algo != CHROMA_ALGO_FREE && !no_square && w.delta_max <= 11) {
+  if (d2 && !partial && !no_square && w.delta_max <= 11) {
     if (w.sq_state == 0) {
+      static const bool ltrace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
+      const auto t0 = std::chrono::steady_clock::now();
       i64 md = 0;
-      w.sq_state = build_square(w.g.rowptr.p, w.g.col.p, w.NL, nullptr, w.sq_rowptr, w.sq_col, md, s) ? 1 : -1;
+      w.sq_state = build_square(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, nullptr, w.sq_rowptr, w.sq_col, md, s) ? 1 : -1;
       w.sq_delta = md;
+      if (ltrace)
+        std::fprintf(stderr, "[square] %s, max degree %lld, %.2f ms\n", w.sq_state == 1 ? "built" : "not applicable",
+                     (long long)md, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
     use_sq = w.sq_state == 1;
   }

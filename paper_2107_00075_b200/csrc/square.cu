@@ -21,12 +21,11 @@
 namespace chroma {
 namespace {
 
-constexpr int SQ_CAP = 128;
 constexpr int SQ_WARPS = 8;
 
 // WRITE = false: row lengths into len (and the max into *maxdeg, overflow into *ovf);
 // WRITE = true: rows into col2 at off.
-template <bool WRITE>
+template <bool WRITE, int SQ_CAP>
 __global__ void __launch_bounds__(SQ_WARPS * 32)
     k_square(const i64* rowptr, const i32* col, i64 nv, const uint8_t* want, i64* len, const i64* off, i32* col2,
              unsigned long long* maxdeg, unsigned* ovf) {
@@ -118,11 +117,13 @@ __global__ void __launch_bounds__(SQ_WARPS * 32)
 
 }  // namespace
 
-// G^2 rows for the vertices with want[v] != 0.  Returns false (nothing built) if a row
-// would exceed SQ_CAP candidates.
-bool build_square(const i64* rowptr, const i32* col, i64 nv, const uint8_t* want, DBuf<i64>& rowptr2,
+// G^2 rows for the vertices with want[v] != 0 (all when want is null).  Returns false
+// (nothing built) if a row would exceed the candidate capacity (128; 64 when the
+// graph's maximum degree d has d + d(d - 1) <= 64).
+bool build_square(const i64* rowptr, const i32* col, i64 nv, i64 delta, const uint8_t* want, DBuf<i64>& rowptr2,
                   DBuf<i32>& col2, i64& maxdeg, cudaStream_t s) {
   if (nv <= 0) return false;
+  const bool small = delta * delta <= 64;
   DBuf<i64> len;
   len.alloc(nv + 1, s);
   DBuf<unsigned long long> md;
@@ -130,7 +131,8 @@ bool build_square(const i64* rowptr, const i32* col, i64 nv, const uint8_t* want
   md.zero(s);
   unsigned* ovf = reinterpret_cast<unsigned*>(md.p + 1);
   const int g = grid_for(nv * 32, SQ_WARPS * 32, num_sms() * 16);
-  k_square<false><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, len.p, nullptr, nullptr, md.p, ovf);
+  if (small) k_square<false, 64><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, len.p, nullptr, nullptr, md.p, ovf);
+  else k_square<false, 128><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, len.p, nullptr, nullptr, md.p, ovf);
   count_launch();
   unsigned long long h[2] = {0, 0};
   CUDA_CHECK(cudaMemcpyAsync(h, md.p, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -143,7 +145,8 @@ bool build_square(const i64* rowptr, const i32* col, i64 nv, const uint8_t* want
   CUDA_CHECK(cudaMemcpyAsync(&total, rowptr2.p + nv, sizeof(i64), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
   col2.alloc(std::max<i64>(total, 1), s);
-  k_square<true><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, nullptr, rowptr2.p, col2.p, md.p, ovf);
+  if (small) k_square<true, 64><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, nullptr, rowptr2.p, col2.p, md.p, ovf);
+  else k_square<true, 128><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, nullptr, rowptr2.p, col2.p, md.p, ovf);
   count_launch();
   CUDA_CHECK(cudaStreamSynchronize(s));
   maxdeg = (i64)h[0];
