@@ -524,8 +524,12 @@ int chroma_world_color(chroma_world* h, int32_t rank, int32_t* colors, const int
     DBuf<i64> nd;
     nd.upload(&nwl, 1, s);
     CUDA_CHECK(cudaMemcpyAsync(w.colors.p + m.lid_off, colors, sizeof(i32) * nl, cudaMemcpyHostToDevice, s));
-    color_csr(w.g.rowptr.p, w.g.col.p, w.NL, w.colors.p, dwl.p, nd.p, nwl, false, dist, partial != 0, algo, false,
-              w.cs, s);
+    const i64* crow = w.g.rowptr.p;
+    const i32* ccol = w.g.col.p;
+    int cdist = dist;
+    i64 cdelta = w.delta_max;
+    square_for(w, dist, partial != 0, crow, ccol, cdist, cdelta);  // distance 2 on a mesh: D1 on G^2
+    color_csr(crow, ccol, w.NL, w.colors.p, dwl.p, nd.p, nwl, false, cdist, partial != 0, algo, false, w.cs, s);
     CUDA_CHECK(cudaMemcpyAsync(colors, w.colors.p + m.lid_off, sizeof(i32) * nl, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
   });

@@ -451,6 +451,33 @@ static void exchange_remote(World& w, bool changed_only) {
 #endif
 }
 
+// Distance 2 without the partial (bipartite) restriction on a bounded-degree graph:
+// the distance-1 kernels on the square G^2 (square.cu) -- identical forbidden sets,
+// orders and loser rule (Gauss-Seidel, Jacobi; the free mode colours such graphs by
+// Gauss-Seidel too).  Detection stays on G.  Builds G^2 on first use; returns whether
+// (crow, ccol, cdist, cdelta) now describe it.
+bool square_for(World& w, int dist, bool partial, const i64*& crow, const i32*& ccol, int& cdist, i64& cdelta) {
+  static const bool no_square = std::getenv("CHROMA_NO_SQUARE") != nullptr;
+  if (dist != 2 || partial || no_square || w.delta_max > 11) return false;
+  if (w.sq_state == 0) {
+    static const bool ltrace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    i64 md = 0;
+    w.sq_state = build_square(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, nullptr, w.sq_rowptr, w.sq_col, md,
+                              w.stream) ? 1 : -1;
+    w.sq_delta = md;
+    if (ltrace)
+      std::fprintf(stderr, "[square] %s, max degree %lld, %.2f ms\n", w.sq_state == 1 ? "built" : "not applicable",
+                   (long long)md, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+  if (w.sq_state != 1) return false;
+  crow = w.sq_rowptr.p;
+  ccol = w.sq_col.p;
+  cdist = 1;
+  cdelta = w.sq_delta;
+  return true;
+}
+
 // ------------------------------------------------------------------ round loop
 int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* colors_out,
                     chroma_round_report* reports, i64* recolored, i64 cap, i64* n_reports,
@@ -525,29 +552,11 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   da.owned_flag = w.owned_flag.p;
   w.det.prev_valid = false;
   const bool remote = w.connected && w.P > 1;
-  // Distance 2 without the partial (bipartite) restriction on a bounded-degree graph:
-  // the distance-1 kernels on the square G^2 (square.cu) -- identical forbidden sets,
-  // orders and loser rule (Gauss-Seidel, Jacobi; the free mode colours such graphs by
-  // Gauss-Seidel too).  Detection stays on G.
-  static const bool no_square = std::getenv("CHROMA_NO_SQUARE") != nullptr;
-  bool use_sq = false;
-  if (d2 && !partial && !no_square && w.delta_max <= 11) {
-    if (w.sq_state == 0) {
-      static const bool ltrace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
-      const auto t0 = std::chrono::steady_clock::now();
-      i64 md = 0;
-      w.sq_state = build_square(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, nullptr, w.sq_rowptr, w.sq_col, md, s) ? 1 : -1;
-      w.sq_delta = md;
-      if (ltrace)
-        std::fprintf(stderr, "[square] %s, max degree %lld, %.2f ms\n", w.sq_state == 1 ? "built" : "not applicable",
-                     (long long)md, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-    }
-    use_sq = w.sq_state == 1;
-  }
-  const i64* crow = use_sq ? w.sq_rowptr.p : w.g.rowptr.p;
-  const i32* ccol = use_sq ? w.sq_col.p : w.g.col.p;
-  const int cdist = use_sq ? 1 : dist;
-  const i64 cdelta = use_sq ? w.sq_delta : w.delta_max;
+  const i64* crow = w.g.rowptr.p;
+  const i32* ccol = w.g.col.p;
+  int cdist = dist;
+  i64 cdelta = w.delta_max;
+  const bool use_sq = square_for(w, dist, partial, crow, ccol, cdist, cdelta);
   if (w.level_n >= 0 && w.level_sq != use_sq) w.level_n = -1;  // a schedule of the other graph
   bool hubs_done = false;
   // CHROMA_ROUND_TRACE[=r]: synchronised per-phase host timings of round r (default 0; dev aid)

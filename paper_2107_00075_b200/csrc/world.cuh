@@ -197,6 +197,7 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
 // Level-synchronous Gauss-Seidel on one thread-block cluster (gs_cluster.cu): the
 // plan is built once from a level schedule (bounded degree <= 32, colours of every
 // vertex fit the cluster's shared memory as bytes); false if not applicable.
+bool square_for(World& w, int dist, bool partial, const i64*& crow, const i32*& ccol, int& cdist, i64& cdelta);
 i64 cluster_max_vertices();
 bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
                         i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s,
