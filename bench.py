@@ -465,7 +465,7 @@ def main():
     kname = {"c3": "k_gs_chunked (chunked exact Gauss-Seidel: throughput first pass + latency-bound dataflow)",
              "c1": "k_gs_cluster (level-synchronous Gauss-Seidel on one cluster)",
              "c2": "k_gs_cluster (level-synchronous Gauss-Seidel on one cluster)",
-             "c4": "gs_kernel<2> (two-hop Gauss-Seidel dataflow)"}.get(wl.name, "round-0 colour phase")
+             "c4": "gs_d1_kernel over the square G^2 (level-ordered Gauss-Seidel; algorithmic bytes counted on G)"}.get(wl.name, "round-0 colour phase")
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
