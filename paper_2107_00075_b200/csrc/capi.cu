@@ -528,7 +528,7 @@ int chroma_world_color(chroma_world* h, int32_t rank, int32_t* colors, const int
     const i32* ccol = w.g.col.p;
     int cdist = dist;
     i64 cdelta = w.delta_max;
-    square_for(w, dist, partial != 0, crow, ccol, cdist, cdelta);  // distance 2 on a mesh: D1 on G^2
+    square_for(w, dist, partial != 0, algo, false, crow, ccol, cdist, cdelta);  // distance 2 as D1 on G^2
     color_csr(crow, ccol, w.NL, w.colors.p, dwl.p, nd.p, nwl, false, cdist, partial != 0, algo, false, w.cs, s);
     CUDA_CHECK(cudaMemcpyAsync(colors, w.colors.p + m.lid_off, sizeof(i32) * nl, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));

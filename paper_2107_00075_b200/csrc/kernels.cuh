@@ -58,9 +58,10 @@ void launch_jacobi_losers(const i64* rowptr, const i32* col, i32* colors, const 
 
 // Edge-based Jacobi sweep (Kernel.EDGE_BASED, distance 1): proposals into prop, the
 // commit, and losers into lose, edge-parallel over the pending rows.
-// the square G^2 over the rows with want[v] (square.cu); false if a row is too long
-bool build_square(const i64* rowptr, const i32* col, i64 nv, i64 delta, const uint8_t* want, DBuf<i64>& rowptr2,
-                  DBuf<i32>& col2, i64& maxdeg, cudaStream_t s);
+// the square G^2 (partial: two-hop only) over the rows with want[v] (square.cu);
+// false if a row is too long or the rows exceed max_entries
+bool build_square(const i64* rowptr, const i32* col, i64 nv, i64 delta, bool partial, i64 max_entries,
+                  const uint8_t* want, DBuf<i64>& rowptr2, DBuf<i32>& col2, i64& maxdeg, cudaStream_t s);
 
 // incremental Jacobi state (jacobi_inc.cu)
 struct JacobiIncScratch {

@@ -456,19 +456,37 @@ static void exchange_remote(World& w, bool changed_only) {
 // orders and loser rule (Gauss-Seidel, Jacobi; the free mode colours such graphs by
 // Gauss-Seidel too).  Detection stays on G.  Builds G^2 on first use; returns whether
 // (crow, ccol, cdist, cdelta) now describe it.
-bool square_for(World& w, int dist, bool partial, const i64*& crow, const i32*& ccol, int& cdist, i64& cdelta) {
+bool square_for(World& w, int dist, bool partial, int algo, bool owned_worklist, const i64*& crow, const i32*& ccol,
+                int& cdist, i64& cdelta) {
   static const bool no_square = std::getenv("CHROMA_NO_SQUARE") != nullptr;
-  if (dist != 2 || partial || no_square || w.delta_max > 11) return false;
+  if (dist != 2 || no_square) return false;
+  // full D2: bounded degree (meshes); PD2: Gauss-Seidel and Jacobi while the two-hop
+  // rows fit in memory (the free mode keeps the net-centric kernels, which read less)
+  if (!partial ? w.delta_max > 11 : (algo == CHROMA_ALGO_FREE || w.delta_max > 128)) return false;
+  // Gauss-Seidel rounds colour owned vertices only: the (large) partial rows of the
+  // ghosts are not needed then
+  const bool owned_only = partial && owned_worklist && algo == CHROMA_ALGO_GAUSS_SEIDEL;
+  const int kind = !partial ? 1 : owned_only ? 3 : 2;
+  if (w.sq_state != 0 && w.sq_kind != kind) {  // another square: rebuild
+    w.sq_state = 0;
+    w.sq_rowptr.release();
+    w.sq_col.release();
+  }
   if (w.sq_state == 0) {
     static const bool ltrace = std::getenv("CHROMA_LEVEL_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
+    size_t free_b = 0, total_b = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const i64 budget = (i64)(free_b / 2 / sizeof(i32));  // at most half the free memory
     i64 md = 0;
-    w.sq_state = build_square(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, nullptr, w.sq_rowptr, w.sq_col, md,
-                              w.stream) ? 1 : -1;
+    w.sq_kind = kind;
+    w.sq_state = build_square(w.g.rowptr.p, w.g.col.p, w.NL, w.delta_max, partial, budget,
+                              owned_only ? w.owned_flag.p : nullptr, w.sq_rowptr, w.sq_col, md, w.stream) ? 1 : -1;
     w.sq_delta = md;
     if (ltrace)
-      std::fprintf(stderr, "[square] %s, max degree %lld, %.2f ms\n", w.sq_state == 1 ? "built" : "not applicable",
-                   (long long)md, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      std::fprintf(stderr, "[square] %s%s, max degree %lld, %.2f ms\n", partial ? "partial, " : "",
+                   w.sq_state == 1 ? "built" : "not applicable", (long long)md,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
   if (w.sq_state != 1) return false;
   crow = w.sq_rowptr.p;
@@ -556,8 +574,9 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
   const i32* ccol = w.g.col.p;
   int cdist = dist;
   i64 cdelta = w.delta_max;
-  const bool use_sq = square_for(w, dist, partial, crow, ccol, cdist, cdelta);
-  if (w.level_n >= 0 && w.level_sq != use_sq) w.level_n = -1;  // a schedule of the other graph
+  const bool use_sq = square_for(w, dist, partial, algo, true, crow, ccol, cdist, cdelta);
+  const int lgraph = use_sq ? w.sq_kind : 0;
+  if (w.level_n >= 0 && w.level_sq != lgraph) w.level_n = -1;  // a schedule of another graph
   bool hubs_done = false;
   // CHROMA_ROUND_TRACE[=r]: synchronised per-phase host timings of round r (default 0; dev aid)
   static const bool round_trace = std::getenv("CHROMA_ROUND_TRACE") != nullptr;
@@ -618,7 +637,7 @@ int run_distributed(World& w, int mode, bool rd, int algo, int max_rounds, i32* 
     // bounded degree (the cluster kernel); other graphs take gs_chunked.cu.
     if (round == 0 && cdist == 1 && gs_like && !no_levels && !hubs_done && cdelta <= 32) {
       if (w.level_n < 0) {
-        w.level_sq = use_sq;
+        w.level_sq = lgraph;
         i64 owned = 0;
         std::vector<i64> counts;
         for (auto& m : w.ranks) {

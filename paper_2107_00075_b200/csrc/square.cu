@@ -21,14 +21,17 @@
 namespace chroma {
 namespace {
 
-constexpr int SQ_WARPS = 8;
+// warps per block: the candidate buffers (SQ_CAP ints per warp) stay within 32 KB
+template <int SQ_CAP>
+constexpr int sq_warps() { return SQ_CAP >= 4096 ? 2 : SQ_CAP >= 2048 ? 4 : 8; }
 
 // WRITE = false: row lengths into len (and the max into *maxdeg, overflow into *ovf);
 // WRITE = true: rows into col2 at off.
-template <bool WRITE, int SQ_CAP>
-__global__ void __launch_bounds__(SQ_WARPS * 32)
+template <bool WRITE, int SQ_CAP, bool PARTIAL>
+__global__ void __launch_bounds__(sq_warps<SQ_CAP>() * 32)
     k_square(const i64* rowptr, const i32* col, i64 nv, const uint8_t* want, i64* len, const i64* off, i32* col2,
              unsigned long long* maxdeg, unsigned* ovf) {
+  constexpr int SQ_WARPS = sq_warps<SQ_CAP>();
   __shared__ i32 cand_all[SQ_WARPS][SQ_CAP];
   __shared__ int ncand_all[SQ_WARPS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -47,9 +50,12 @@ __global__ void __launch_bounds__(SQ_WARPS * 32)
     bool over = false;
     for (i64 e = rs + lane; e < re; e += 32) {
       const i32 u = col[e];
-      int k = atomicAdd(&ncand, 1);
-      if (k < SQ_CAP) cand[k] = u;
-      else over = true;
+      int k;
+      if (!PARTIAL) {  // partial distance 2: the middles themselves are not forbidden
+        k = atomicAdd(&ncand, 1);
+        if (k < SQ_CAP) cand[k] = u;
+        else over = true;
+      }
       for (i64 f = rowptr[u]; f < rowptr[u + 1]; f++) {
         const i32 x = col[f];
         if (x == (i32)v) continue;
@@ -67,13 +73,15 @@ __global__ void __launch_bounds__(SQ_WARPS * 32)
       continue;
     }
     const int K = ncand;
-    // bitonic sort of the (padded) candidates, then the first of each run is kept
-    for (int i = lane; i < SQ_CAP; i += 32)
-      if (i >= K) cand[i] = INT32_MAX;
+    // bitonic sort of the candidates padded to the next power of two (>= 64), then the
+    // first of each run is kept
+    int n2 = 64;
+    while (n2 < K) n2 <<= 1;
+    for (int i = K + lane; i < n2; i += 32) cand[i] = INT32_MAX;
     __syncwarp();
-    for (int k = 2; k <= SQ_CAP; k <<= 1)
+    for (int k = 2; k <= n2; k <<= 1)
       for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < SQ_CAP; i += 32) {
+        for (int i = lane; i < n2; i += 32) {
           const int ixj = i ^ j;
           if (ixj > i) {
             const i32 a = cand[i], b = cand[ixj];
@@ -85,15 +93,10 @@ __global__ void __launch_bounds__(SQ_WARPS * 32)
         }
         __syncwarp();
       }
-    constexpr int PER = SQ_CAP / 32;
-    bool keep[PER];
+    const int PER = n2 / 32;  // lane l keeps positions [l * PER, (l + 1) * PER)
+    auto keep = [&](int i) { return cand[i] != INT32_MAX && (i == 0 || cand[i] != cand[i - 1]); };
     int mine = 0;
-#pragma unroll
-    for (int q = 0; q < PER; q++) {
-      const int i = lane * PER + q;
-      keep[q] = cand[i] != INT32_MAX && (i == 0 || cand[i] != cand[i - 1]);
-      mine += keep[q];
-    }
+    for (int q = 0; q < PER; q++) mine += keep(lane * PER + q);
     if (WRITE) {
       int inc = mine;
 #pragma unroll
@@ -102,9 +105,8 @@ __global__ void __launch_bounds__(SQ_WARPS * 32)
         if (lane >= o) inc += t;
       }
       i64 at = off[v] + inc - mine;
-#pragma unroll
       for (int q = 0; q < PER; q++)
-        if (keep[q]) col2[at++] = cand[lane * PER + q];
+        if (keep(lane * PER + q)) col2[at++] = cand[lane * PER + q];
     }
     const int U = __reduce_add_sync(0xffffffffu, mine);
     if (!WRITE && lane == 0) {
@@ -115,39 +117,63 @@ __global__ void __launch_bounds__(SQ_WARPS * 32)
   }
 }
 
+template <bool W, int CAP>
+void launch_square(bool partial, const i64* rowptr, const i32* col, i64 nv, const uint8_t* want, i64* len,
+                   const i64* off, i32* col2, unsigned long long* md, unsigned* ovf, cudaStream_t s) {
+  constexpr int T = sq_warps<CAP>() * 32;
+  const int g = grid_for(nv * 32, T, num_sms() * 16);
+  if (partial) k_square<W, CAP, true><<<g, T, 0, s>>>(rowptr, col, nv, want, len, off, col2, md, ovf);
+  else k_square<W, CAP, false><<<g, T, 0, s>>>(rowptr, col, nv, want, len, off, col2, md, ovf);
+  count_launch();
+}
+
+template <bool W>
+void launch_square_cap(int cap, bool partial, const i64* rowptr, const i32* col, i64 nv, const uint8_t* want,
+                       i64* len, const i64* off, i32* col2, unsigned long long* md, unsigned* ovf, cudaStream_t s) {
+  if (cap == 64) launch_square<W, 64>(partial, rowptr, col, nv, want, len, off, col2, md, ovf, s);
+  else if (cap == 128) launch_square<W, 128>(partial, rowptr, col, nv, want, len, off, col2, md, ovf, s);
+  else if (cap == 2048) launch_square<W, 2048>(partial, rowptr, col, nv, want, len, off, col2, md, ovf, s);
+  else launch_square<W, 4096>(partial, rowptr, col, nv, want, len, off, col2, md, ovf, s);
+}
+
 }  // namespace
 
-// G^2 rows for the vertices with want[v] != 0 (all when want is null).  Returns false
-// (nothing built) if a row would exceed the candidate capacity (128; 64 when the
-// graph's maximum degree d has d + d(d - 1) <= 64).
-bool build_square(const i64* rowptr, const i32* col, i64 nv, i64 delta, const uint8_t* want, DBuf<i64>& rowptr2,
-                  DBuf<i32>& col2, i64& maxdeg, cudaStream_t s) {
+// G^2 (partial: two-hop only, the PD2 forbidden set) rows for the vertices with
+// want[v] != 0 (all when want is null).  Returns false (nothing built) if a row would
+// exceed the candidate capacity, or the rows would exceed max_entries in total.  The
+// capacity follows the graph's maximum degree d: 64 when d + d(d - 1) <= 64, 128 up
+// to d = 11, else 2048, retried at 4096 if a row overflows; each row sorts only the
+// next power of two above its candidate count.
+bool build_square(const i64* rowptr, const i32* col, i64 nv, i64 delta, bool partial, i64 max_entries,
+                  const uint8_t* want, DBuf<i64>& rowptr2, DBuf<i32>& col2, i64& maxdeg, cudaStream_t s) {
   if (nv <= 0) return false;
-  const bool small = delta * delta <= 64;
+  int cap = delta * delta <= 64 ? 64 : delta <= 11 ? 128 : 2048;
   DBuf<i64> len;
   len.alloc(nv + 1, s);
   DBuf<unsigned long long> md;
   md.alloc(2, s);
-  md.zero(s);
   unsigned* ovf = reinterpret_cast<unsigned*>(md.p + 1);
-  const int g = grid_for(nv * 32, SQ_WARPS * 32, num_sms() * 16);
-  if (small) k_square<false, 64><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, len.p, nullptr, nullptr, md.p, ovf);
-  else k_square<false, 128><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, len.p, nullptr, nullptr, md.p, ovf);
-  count_launch();
   unsigned long long h[2] = {0, 0};
-  CUDA_CHECK(cudaMemcpyAsync(h, md.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  if (h[1] & 0xffffffffull) return false;
+  for (;;) {  // the wide capacity (fewer warps per SM) only if a row needs it
+    md.zero(s);
+    launch_square_cap<false>(cap, partial, rowptr, col, nv, want, len.p, nullptr, nullptr, md.p, ovf, s);
+    CUDA_CHECK(cudaMemcpyAsync(h, md.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (!(h[1] & 0xffffffffull)) break;
+    if (cap != 2048) return false;
+    cap = 4096;
+  }
   CUDA_CHECK(cudaMemsetAsync(len.p + nv, 0, sizeof(i64), s));
-  rowptr2.alloc(nv + 1, s);
-  exclusive_scan_i64(len.p, rowptr2.p, nv + 1, s);
+  DBuf<i64> rp;
+  rp.alloc(nv + 1, s);
+  exclusive_scan_i64(len.p, rp.p, nv + 1, s);
   i64 total = 0;
-  CUDA_CHECK(cudaMemcpyAsync(&total, rowptr2.p + nv, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaMemcpyAsync(&total, rp.p + nv, sizeof(i64), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
+  if (total > max_entries || total >= ((i64)1 << 31) * 4) return false;
+  rowptr2 = std::move(rp);
   col2.alloc(std::max<i64>(total, 1), s);
-  if (small) k_square<true, 64><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, nullptr, rowptr2.p, col2.p, md.p, ovf);
-  else k_square<true, 128><<<g, SQ_WARPS * 32, 0, s>>>(rowptr, col, nv, want, nullptr, rowptr2.p, col2.p, md.p, ovf);
-  count_launch();
+  launch_square_cap<true>(cap, partial, rowptr, col, nv, want, nullptr, rowptr2.p, col2.p, md.p, ovf, s);
   CUDA_CHECK(cudaStreamSynchronize(s));
   maxdeg = (i64)h[0];
   return true;

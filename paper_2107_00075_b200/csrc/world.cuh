@@ -146,11 +146,12 @@ struct World {
   DBuf<i32> level_wl;
   i64 level_n = -1;
   bool level_mode = false;
-  bool level_sq = false;  // the schedule is of the square (distance-2 runs)
+  int level_sq = 0;  // the schedule is of G (0) or of the square of that kind (sq_kind)
   ClusterPlan cplan;
   // the square of the local graph (square.cu), built on the first
   // distance-2 run of a bounded-degree world: 0 not yet, 1 built, -1 not applicable
   int sq_state = 0;
+  int sq_kind = 0;  // 1 square, 2 partial square (two-hop only), 3 partial square of the owned rows
   DBuf<i64> sq_rowptr;
   DBuf<i32> sq_col;
   i64 sq_delta = 0;
@@ -197,7 +198,8 @@ bool build_level_order(const i64* rowptr, const i32* col, i64 nv, const i32* wl,
 // Level-synchronous Gauss-Seidel on one thread-block cluster (gs_cluster.cu): the
 // plan is built once from a level schedule (bounded degree <= 32, colours of every
 // vertex fit the cluster's shared memory as bytes); false if not applicable.
-bool square_for(World& w, int dist, bool partial, const i64*& crow, const i32*& ccol, int& cdist, i64& cdelta);
+bool square_for(World& w, int dist, bool partial, int algo, bool owned_worklist, const i64*& crow, const i32*& ccol,
+                int& cdist, i64& cdelta);
 i64 cluster_max_vertices();
 bool build_cluster_plan(const i64* rowptr, const i32* col, i64 nv, i64 max_deg, const i32* level_wl,
                         i64 level_n, const std::vector<i64>& level_sizes, ClusterPlan& plan, cudaStream_t s,

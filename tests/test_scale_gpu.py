@@ -86,8 +86,6 @@ def test_deterministic_bit_exact(key, run_key):
     mode, P = run_key.rsplit("_p", 1)
     P, _, alg = P.partition("_")
     ref = SCALE[key][run_key]
-    if mode == "pd2" and key == "c5_2p22":
-        pytest.skip("deterministic PD2 at 2^22 is checked at 2^20 (c5_2p20); 2^22 runs free-mode below")
     g = graph(key)
     colors, reports = run(g, mode, int(P), algorithm=alg or None)
     assert sha(colors) == ref["sha256"]
