@@ -211,6 +211,16 @@ def round0_bytes(n_owned: int, nnz_owned: int, touched: int) -> int:
     return 4 * n_owned + 8 * (n_owned + 1) + 4 * nnz_owned + 4 * touched
 
 
+def gather_rate():
+    """Measured random-load rate of this GPU type (L2-resident int32 array, 16 loads in
+    flight per thread): profiles/gather_roofline.json, written by scripts/gather_roofline.cu."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_roofline.json")) as fh:
+            return float(json.loads(fh.readline())["gather_i32_64MB"]["gathers_per_s"])
+    except Exception:
+        return None
+
+
 def sha256_i32(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).astype("<i4").tobytes()).hexdigest()
 
@@ -448,6 +458,26 @@ def main():
                    "oracle_sha256": jref.get("sha256"),
                    "match": (jref.get("sha256") == jsha) if jref.get("sha256") else None,
                    "oracle_run_s": jref.get("oracle_run_s")}
+    # ---- the checker (verify_d1 count, k_count_d1) on the headline's device colours, C3 at N=1
+    ver = None
+    if rank == 0 and N == 1 and wl.name == "c3" and not args.no_free:
+        R.run_distributed(world, cfg, out=out)
+        h = _lib.csr_of(g)
+        nv = C.c_int64(0)
+        vt = []
+        for _ in range(4):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _lib.check(_lib.lib().chroma_verify(h.h, C.c_void_p(out.data_ptr()), None, 0, C.byref(nv), None, 0,
+                                                1), "verify")
+            vt.append(time.perf_counter() - t0)
+        tv = min(vt[1:])
+        rate = gather_rate()
+        ver = {"ms": 1e3 * tv, "violations": int(nv.value), "edges_per_s": m / tv,
+               "timing": "host perf_counter around chroma_verify (device colours, count only), best of 3 after 1",
+               "gather_floor_ms": 1e3 * m / rate if rate else None,
+               "gather_frac": (m / rate) / tv if rate else None,
+               "note": "one random colour load per edge (u > v), L1-wavefront bound (profiles/gather_roofline.json)"}
     # ---- roofline of the dominant kernel (the round-0 colouring)
     n_o = lg.owned_count
     nnz_o = int(lg.row_offsets[n_o]) if N > 1 else len(g.col_indices)
@@ -466,6 +496,17 @@ def main():
              "c1": "k_gs_cluster (level-synchronous Gauss-Seidel on one cluster)",
              "c2": "k_gs_cluster (level-synchronous Gauss-Seidel on one cluster)",
              "c4": "gs_d1_kernel over the square G^2 (level-ordered Gauss-Seidel; algorithmic bytes counted on G)"}.get(wl.name, "round-0 colour phase")
+    # second roofline: random neighbour-colour loads retire at ~1 per SM clock from L2
+    # (one L1 wavefront each; scripts/gather_roofline.cu), so a colouring pass that loads
+    # each lower neighbour's colour once has a floor of (lower entries) / (gather rate)
+    gather_roof = None
+    rate = gather_rate()
+    if rate and wl.name == "c3":
+        lower = m if N == 1 else nnz_o // 2
+        gather_roof = {"gathers_per_launch": lower, "rate_per_s": rate,
+                       "floor_ms": 1e3 * lower / rate, "frac": (lower / rate) / kernel_s if kernel_s > 0 else None,
+                       "gathers": "one colour load per lower neighbour (round 0 reads rows up to the vertex)"
+                                  + ("" if N == 1 else "; nnz_owned / 2 at N > 1")}
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -523,11 +564,11 @@ def main():
                                       if wl.name == "c3" else "per-world round-0 schedule built in warm-up",
                            "cold_call_ms": cold_ms,
                            "l2": f"inputs larger than L2 (int32 col {4 * len(g.col_indices) / 1e6:.0f} MB)"},
-                "parity": parity, "free": free, "jacobi": jac,
+                "parity": parity, "free": free, "jacobi": jac, "verify": ver,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak if achieved else None, "traffic": traffic,
                              "kernel": kname, "algorithmic_bytes_per_launch": B, "kernel_ms": kernel_s * 1e3,
-                             "peak_kind": peak_kind},
+                             "peak_kind": peak_kind, "gather": gather_roof},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
         emit(line)
     if N > 1:

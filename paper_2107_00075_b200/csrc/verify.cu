@@ -7,6 +7,7 @@
 // find equal-colour groups in one step); listing re-walks only the rows that have
 // violations and writes them at exclusive-scan offsets, which reproduces the
 // reference's ordering without a sort.
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.cuh"
@@ -118,56 +119,139 @@ __global__ void k_rows(VArgs a, i64* cnt, const i64* off, i64 base_pos, i64 cap,
 }
 
 // Count-only verify_d1 (no listing): uncoloured vertices plus equal-coloured edges
-// (u, v > u).  A warp takes 32 consecutive rows: a lane walks a row of <= 32 entries
-// alone (8 column loads in flight), the warp walks the longer ones; one atomic per
-// warp at the end.  Reads rowptr, col and the colour of every neighbour once.
-__global__ void k_count_d1(VArgs a, unsigned long long* total) {
-  const int lane = threadIdx.x & 31;
-  const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
-  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+// (u, v > u).  Edge-tiled so the column stream is read with full-width coalesced loads
+// whatever the degree skew: a CTA takes a tile of VT_TILE consecutive entries, stages
+// the tile's slice of rowptr in shared memory (tile start rows from one pass over
+// rowptr, loaded a tile ahead), and each
+// thread takes VT_PER consecutive entries (two 16-byte loads), finds their rows by a
+// binary search in shared memory and gathers the neighbours' colours from a 16-bit
+// copy of the colour array.  The random colour loads bound it (one L1 wavefront each,
+// ~1 per SM clock: scripts/gather_roofline.cu), so occupancy carries it.
+// Colours >= 0xFFFF saturate in the copy; a saturated match re-checks the int32 colours.
+// Reads rowptr, col and every neighbour's colour once (B = 8(n+1) + 4 nnz + 4n + 2 nnz
+// gathered halfwords).
+constexpr int VT_THREADS = 256;
+constexpr int VT_PER = 8;
+constexpr int VT_TILE = VT_THREADS * VT_PER;
+constexpr int VT_MINB = 6;  // <= 40 registers: occupancy carries the gathers (A/B on C3:
+                            // 8 entries x 6 CTAs 1.73 ms; 16 x 3 2.4 ms; 4 x 8 1.9 ms; row-wise 2.2 ms)
+constexpr int VT_ROWS = 2048;  // rows of a tile staged in shared memory (more: global search)
+
+__global__ void k_colors16(const i32* colors, i64 n, uint16_t* c16, unsigned long long* total) {
+  unsigned long long zeros = 0;
+  for (i64 v = blockIdx.x * (i64)blockDim.x + threadIdx.x; v < n; v += (i64)gridDim.x * blockDim.x) {
+    const i32 c = __ldcs(colors + v);
+    c16[v] = (uint16_t)(c < 0 ? 0xFFFF : c > 0xFFFE ? 0xFFFF : c);
+    zeros += c == 0;
+  }
+  zeros = __reduce_add_sync(FULL, (unsigned)zeros);
+  if ((threadIdx.x & 31) == 0 && zeros) atomicAdd(total, zeros);
+}
+
+// largest r in [lo, hi] with rp[r] <= e
+__device__ __forceinline__ i64 row_search(const i64* rp, i64 lo, i64 hi, i64 e) {
+  while (lo < hi) {
+    const i64 mid = (lo + hi + 1) >> 1;
+    if (__ldg(rp + mid) <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// tile_row[t] = the row holding entry t * VT_TILE (t < ntiles), tile_row[ntiles] = n - 1:
+// each non-empty row writes the tiles that start inside it (one pass over rowptr)
+__global__ void k_tile_rows(const i64* rp, i64 n, i64 ntiles, i32* tile_row) {
+  for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < n; r += (i64)gridDim.x * blockDim.x) {
+    const i64 rs = __ldg(rp + r), re = __ldg(rp + r + 1);
+    for (i64 t = (rs + VT_TILE - 1) / VT_TILE; t * VT_TILE < re; t++) tile_row[t] = (i32)r;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) tile_row[ntiles] = (i32)(n - 1);
+}
+
+__global__ void __launch_bounds__(VT_THREADS, VT_MINB) k_count_d1(const i64* rp, const i32* col, i64 n, const i32* tile_row,
+                                                         const uint16_t* c16, const i32* c32, bool aligned,
+                                                         unsigned long long* total) {
+  __shared__ i32 s_off[VT_ROWS + 1];
+  const i64 nnz = n > 0 ? __ldg(rp + n) : 0;
   unsigned long long mine = 0;
-  for (i64 b = warp * 32; b < a.n; b += nwarps * 32) {
-    const i64 r = b + lane;
-    i32 cu = 0;
-    i64 rs = 0, re = 0;
-    if (r < a.n) {
-      cu = a.colors[r];
-      rs = a.rowptr[r];
-      re = a.rowptr[r + 1];
-      if (cu == 0) {
-        mine++;
-        re = rs;
+  // the next tile's row range is loaded one tile ahead, its columns before the staging
+  i64 nlo = 0, nhi = 0;
+  if ((i64)blockIdx.x * VT_TILE < nnz) {
+    nlo = __ldg(tile_row + blockIdx.x);
+    nhi = __ldg(tile_row + blockIdx.x + 1);
+  }
+  for (i64 t = blockIdx.x; t * VT_TILE < nnz; t += gridDim.x) {
+    const i64 e0 = t * VT_TILE;
+    const i64 e1 = min(e0 + (i64)VT_TILE, nnz);
+    const int x0 = threadIdx.x * VT_PER;
+    const int len = (int)(e1 - e0);
+    i32 us[VT_PER];
+    if (aligned && x0 + VT_PER <= len) {
+      const int4* p4 = reinterpret_cast<const int4*>(col + e0 + x0);
+#pragma unroll
+      for (int q = 0; q < VT_PER / 4; q++) {
+        const int4 w = __ldcs(p4 + q);
+        us[4 * q] = w.x; us[4 * q + 1] = w.y; us[4 * q + 2] = w.z; us[4 * q + 3] = w.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < VT_PER; q++) us[q] = x0 + q < len ? __ldcs(col + e0 + x0 + q) : -1;
+    }
+    const i64 rlo = nlo, rhi = nhi;
+    const i64 tn = t + gridDim.x;
+    if (tn * VT_TILE < nnz) {
+      nlo = __ldg(tile_row + tn);
+      nhi = __ldg(tile_row + tn + 1);
+    }
+    const i64 nr = rhi - rlo + 1;
+    const bool fits = nr <= VT_ROWS;
+    if (fits) {
+      for (i64 i = threadIdx.x; i <= nr; i += VT_THREADS) {
+        const i64 o = __ldg(rp + rlo + i) - e0;
+        s_off[i] = (i32)(o < 0 ? 0 : o > VT_TILE ? VT_TILE : o);
       }
     }
-    const bool lng = re - rs > 32;
-    if (!lng) {
-      for (i64 e0 = rs; e0 < re; e0 += 8) {
-        i32 vs[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) vs[q] = e0 + q < re ? __ldcs(a.col + e0 + q) : -1;
-#pragma unroll
-        for (int q = 0; q < 8; q++) mine += (vs[q] > r && a.colors[vs[q]] == cu) ? 1 : 0;
-      }
-    }
-    for (unsigned lm = __ballot_sync(FULL, lng); lm; lm &= lm - 1) {
-      const int src = __ffs(lm) - 1;
-      const i64 rr = b + src;
-      const i32 cl = __shfl_sync(FULL, cu, src);
-      const i64 ls = __shfl_sync(FULL, rs, src), le = __shfl_sync(FULL, re, src);
-      for (i64 e0 = ls; e0 < le; e0 += 128) {
-        i32 vs[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const i64 e = e0 + q * 32 + lane;
-          vs[q] = e < le ? __ldcs(a.col + e) : -1;
+    __syncthreads();
+    if (x0 < len) {
+      // row (relative to rlo) of the first entry, then walk the row boundaries
+      i64 ri;
+      if (fits) {
+        int lo = 0, hi = (int)nr - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_off[mid] <= x0) lo = mid;
+          else hi = mid - 1;
         }
+        ri = lo;
+      } else {
+        ri = row_search(rp, rlo, rhi, e0 + x0) - rlo;
+      }
+      auto off_at = [&](i64 i) -> i64 { return fits ? (i64)s_off[i] : min(__ldg(rp + rlo + i) - e0, (i64)VT_TILE); };
+      i64 nxt = off_at(ri + 1);
+      i32 rows[VT_PER];
 #pragma unroll
-        for (int q = 0; q < 4; q++) mine += (vs[q] > rr && a.colors[vs[q]] == cl) ? 1 : 0;
+      for (int q = 0; q < VT_PER; q++) {
+        while (x0 + q >= nxt && x0 + q < len) nxt = off_at(++ri + 1);
+        rows[q] = (i32)(rlo + ri);
+      }
+      // one gather per neighbour (each costs an L1 wavefront: ~1 per SM clock, measured
+      // in scripts/gather_roofline.cu); the row's own colour once per row
+      uint16_t cu[VT_PER], cv[VT_PER];
+#pragma unroll
+      for (int q = 0; q < VT_PER; q++) {
+        const bool live = us[q] > rows[q];
+        cv[q] = live ? __ldg(c16 + us[q]) : 0;
+        cu[q] = q > 0 && rows[q] == rows[q - 1] ? cu[q - 1] : __ldg(c16 + rows[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < VT_PER; q++) {
+        if (cu[q] != 0 && cu[q] == cv[q]) mine += cu[q] != 0xFFFF || __ldg(c32 + us[q]) == __ldg(c32 + rows[q]);
       }
     }
+    __syncthreads();
   }
   mine = __reduce_add_sync(FULL, (unsigned)mine);
-  if (lane == 0 && mine) atomicAdd(total, mine);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(total, mine);
 }
 
 __global__ void k_write_uncolored(const i32* ids, const i64* nsel, i64 cap, i64* out) {
@@ -191,7 +275,20 @@ i64 run_verify(const i64* rowptr, const i32* col, i64 n, const i32* colors, cons
     DBuf<unsigned long long> t;
     t.alloc(1, s);
     t.zero(s);
-    k_count_d1<<<grid_for(n, 256, num_sms() * 16), 256, 0, s>>>(a, t.p);
+    DBuf<uint16_t> c16;
+    c16.alloc(n + 1, s);
+    k_colors16<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(colors, n, c16.p, t.p);
+    count_launch();
+    const bool aligned = (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+    i64 nnz = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&nnz, rowptr + n, sizeof(i64), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    const i64 ntiles = (nnz + VT_TILE - 1) / VT_TILE;
+    DBuf<i32> trow;
+    trow.alloc(ntiles + 1, s);
+    k_tile_rows<<<grid_for(n, 256, num_sms() * 8), 256, 0, s>>>(rowptr, n, ntiles, trow.p);
+    count_launch();
+    k_count_d1<<<num_sms() * 12, VT_THREADS, 0, s>>>(rowptr, col, n, trow.p, c16.p, colors, aligned, t.p);
     count_launch();
     unsigned long long h = 0;
     CUDA_CHECK(cudaMemcpyAsync(&h, t.p, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -150,9 +150,43 @@ def cmd_dist(args):
     dist.destroy_process_group()
 
 
+def cmd_verify(args):
+    """Count-only checker (verify_d1) on the device colours of a deterministic run:
+    CUDA-event time per chroma_verify call and its violation count."""
+    import torch
+    from paper_2107_00075_b200 import _lib
+    from paper_2107_00075_b200 import partition as PT
+    from paper_2107_00075_b200 import protocol as R
+    from paper_2107_00075_b200 import runtime as RT
+    g, mode = make_graph(args.graph)
+    w = RT.build_local_graphs(g, PT.partition_block(g, 1), R.ghost_layers_for(mode))
+    out = torch.empty(g.num_vertices, dtype=torch.int32, device="cuda")
+    R.run_distributed(w, R.AlgorithmConfig(mode=mode, deterministic=True), out=out)
+    del w
+    h = _lib.csr_of(g)
+    vm = 0 if mode in (R.Mode.D1, R.Mode.D1_2GL) else (2 if mode is R.Mode.PD2 else 1)
+    nv = C.c_int64(0)
+    rows = np.zeros((1, 4), np.int64)
+    for bad in (False, True):
+        if bad:  # random colours 0..7: many violations; the listing path must count the same
+            out = torch.randint(0, 8, (g.num_vertices,), dtype=torch.int32, device="cuda",
+                                generator=torch.Generator("cuda").manual_seed(7))
+        ts = []
+        for _ in range(args.reps):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            _lib.check(_lib.lib().chroma_verify(h.h, C.c_void_p(out.data_ptr()), None, vm, C.byref(nv), None, 0, 1))
+            ts.append((time.perf_counter() - t) * 1e3)
+        cnt = nv.value
+        _lib.check(_lib.lib().chroma_verify(h.h, C.c_void_p(out.data_ptr()), None, vm, C.byref(nv),
+                                            _lib.ptr(rows), 1, 1))
+        print(f"{args.graph} verify{'(random colours)' if bad else ''}: violations {cnt} (listing path {nv.value}), "
+              f"ms {' '.join(f'{x:.3f}' for x in ts)}", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
-    ap.add_argument("cmd", choices=["run", "e2e", "dist"])
+    ap.add_argument("cmd", choices=["run", "e2e", "dist", "verify"])
     ap.add_argument("--graph", default="c3")
     ap.add_argument("--P", default="1")
     ap.add_argument("--algo", default="gs")
@@ -161,7 +195,7 @@ def main():
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--e2e", action="store_true")
     args = ap.parse_args()
-    {"run": cmd_run, "e2e": cmd_e2e, "dist": cmd_dist}[args.cmd](args)
+    {"run": cmd_run, "e2e": cmd_e2e, "dist": cmd_dist, "verify": cmd_verify}[args.cmd](args)
 
 
 if __name__ == "__main__":

@@ -110,7 +110,8 @@ def test_free_d2_proper(mode, builder, P):
     colors, ref, reports = _run(g, mode, P)
     _check_proper(g, colors, mode)
     assert reports[-1].conflicts == 0
-    assert colors.max() <= 1.5 * ref.max()
+    # north_star: within 5 % of the deterministic colour count (+1 for small palettes)
+    assert colors.max() <= 1.05 * ref.max() + 1, (colors.max(), ref.max())
 
 
 def test_free_isolated_and_empty_rows():

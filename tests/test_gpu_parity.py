@@ -182,12 +182,36 @@ def test_verify_and_stats(golden_runs, golden_arrays):
                 arr = np.array([[kinds[v.kind], v.u, -1 if v.w is None else v.w,
                                  -1 if v.middle is None else v.middle] for v in viol], dtype=np.int64).reshape(-1, 4)
                 assert np.array_equal(arr, golden_arrays[f"{base}/{label}"].astype(np.int64)), (base, label)
+            # the count-only checker (edge-tiled kernel) agrees with the golden listing
+            assert V.count_violations(g, c, "d1") == len(got["d1"]), base
             n_c, hist = V.color_stats(c)
             assert n_c == stats[base + "/stats"]["num_colors"]
             assert {str(k): v for k, v in hist.items()} == stats[base + "/stats"]["hist"]
         assert np.array_equal(L.serial_greedy(g), golden_arrays[f"serial/{case}/natural"])
         order = golden_arrays[f"serial/{case}/order"].astype(np.int64)
         assert np.array_equal(L.serial_greedy(g, order), golden_arrays[f"serial/{case}/ordered"])
+
+
+@pytest.mark.parametrize("case", ["rmat", "star", "isolated", "empty"])
+def test_count_violations_matches_listing(case):
+    """count_violations (edge tiles of 4096 entries, 16-bit colour copy) against the
+    listing path: skewed rows, tiles spanning thousands of one-entry rows, isolated
+    vertices, colours above 0xFFFE (saturated in the copy)."""
+    rng = np.random.default_rng(5)
+    if case == "rmat":
+        g = G.gen_rmat(14, 16, 3)
+    elif case == "star":  # vertex 0 joined to 1..6000: tiles over 6000 one-entry rows
+        n = 9000
+        g = G.preprocess(n, np.stack([np.zeros(6000, np.int64), np.arange(1, 6001)], 1))
+    elif case == "isolated":
+        g = G.preprocess(50000, rng.integers(0, 50000, size=(3000, 2)))
+    else:
+        g = G.Graph(10, np.zeros(11, np.int64), np.zeros(0, np.int64))
+    for palette in (3, 7, 1 << 17):
+        c = rng.integers(0, palette, size=g.num_vertices).astype(np.int32)
+        if palette > 0xFFFF and g.num_vertices > 4:  # equal and unequal colours above 0xFFFE
+            c[:4] = [0xFFFF, 0x1FFFF, 0xFFFF, 0x10000]
+        assert V.count_violations(g, c, "d1") == len(V.verify_d1(g, c)), (case, palette)
 
 
 # ------------------------------------------------------------------ seeded random vs the C oracle
