@@ -410,6 +410,10 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
     // (previous chunk) and before its next writer (next chunk)
     unsigned* const bc = a.cnt + (((a0 / a.chunk) & 1) ? 3 : 0);
     unsigned* const bc_next = a.cnt + (((a0 / a.chunk) & 1) ? 0 : 3);
+    // first-pass (2) items are grabbed dynamically (rows differ widely in length):
+    // [0] warp rows, [1] hub slices, [2] group rows (quads); same parity scheme
+    unsigned* const gc = a.cnt + (((a0 / a.chunk) & 1) ? 11 : 8);
+    unsigned* const gc_next = a.cnt + (((a0 / a.chunk) & 1) ? 8 : 11);
     const i64 a1 = a0 + a.chunk < a.nwl ? a0 + a.chunk : a.nwl;
     const i32 s0 = a.wl[a0];
     const i64 ngroups = (a1 - a0 + 31) / 32;
@@ -463,7 +467,12 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
       // hub rows: every slice by one CTA; partial results meet in the hub's slot and
       // the CTA that finishes the last slice finishes the row
       __shared__ int last;
-      for (unsigned h = blockIdx.x; h < nc; h += gridDim.x) {
+      __shared__ unsigned item;
+      for (;;) {
+        if (threadIdx.x == 0) item = atomicAdd(gc + 1, 1u);
+        __syncthreads();
+        const unsigned h = item;
+        if (h >= nc) break;
         const i32 vh = __ldcg(a.big[1] + h);
         const int2 it = __ldcg(a.slice + h);
         const i64 rs = a.rowptr[vh], re = a.rowptr[vh + 1];
@@ -517,7 +526,11 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
         }
         __syncthreads();
       }
-      for (i64 h = gw; h < nwr; h += nwarps) {
+      for (;;) {
+        unsigned h = 0;
+        if (lane == 0) h = atomicAdd(gc + 0, 1u);
+        h = __shfl_sync(FULLM, h, 0);
+        if (h >= nwr) break;
         const i32 vl = __ldcg(a.big[0] + h);
         bm[lane] = 0;
         if (lane == 0) wlen[wid] = 0;
@@ -541,7 +554,11 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
         const int slot = wid * NG + g;
         u32* gbm = lbm_all + slot * CF_WORDS;
         i32* glist = (i32*)lbm_all + CF_WARPS * NG * CF_WORDS + slot * CF_OPEN;
-        for (i64 h0 = gw * NG; h0 < nmed; h0 += nwarps * NG) {
+        for (;;) {
+          unsigned h0 = 0;
+          if (lane == 0) h0 = atomicAdd(gc + 2, (unsigned)NG);
+          h0 = __shfl_sync(FULLM, h0, 0);
+          if (h0 >= nmed) break;
           const i64 h = h0 + g;
           if (h < nmed) {
             const i32 vm = __ldcg(a.big[2] + h);
@@ -563,7 +580,10 @@ __global__ void __launch_bounds__(CF_THREADS, 1) k_gs_chunked(CfArgs a) {
     grid.sync();
     tr(2, 0);
     // ---------------- dataflow over the open vertices
-    if (blockIdx.x == 0 && threadIdx.x < 3) bc_next[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < 3) {
+      bc_next[threadIdx.x] = 0;
+      gc_next[threadIdx.x] = 0;
+    }
     if (wid < CF_HUBW) {
       // hub warps: this warp's hubs of the chunk, ascending
       const unsigned nh = __ldcg(bc + 1);
@@ -682,7 +702,7 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
   S.hub_open.reserve(hub_cap * CF_HUB_OPEN, s);
   S.hub_top.reserve(1, s);
   CUDA_CHECK(cudaMemsetAsync(S.hub_top.p, 0, sizeof(unsigned), s));
-  S.cnt.reserve(8, s);
+  S.cnt.reserve(16, s);
   S.cnt.zero(s);
   S.desc.reserve(nv, s);
   const i64 nnz = nnz_all;
