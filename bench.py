@@ -546,7 +546,8 @@ def main():
                "d2h_bytes_per_step": int(4 * n_out),
                "timing": "host perf_counter around build_local_graphs (int64 CSR from pageable NumPy arrays "
                          "to the device world) + run_distributed (colours back into host memory)",
-               "pinned_value": m / te}
+               "pinned_value": m / te,
+               "host_cores": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()}
         del pg
         del off_p, col_p
     cpu = None
