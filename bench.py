@@ -539,7 +539,7 @@ def main():
         K = max(1, min(args.steps, 3))
         # the drop-in caller's input: plain (pageable) NumPy int64 arrays
         pg = Graph(g.num_vertices, np.array(g.row_offsets, np.int64), np.array(g.col_indices, np.int64))
-        tp = e2e_steps(pg, PT.partition_block(pg, N), K, max(1, min(args.warmup, 2)))
+        tp = e2e_steps(pg, PT.partition_block(pg, N), K, max(1, min(args.warmup, 3)))
         te = e2e_steps(hg, hpm, K, 1)
         e2e = {"value": m / tp, "unit": UNIT,
                "h2d_bytes_per_step": int(off_p.numel() * 8 + col_p.numel() * 8),
