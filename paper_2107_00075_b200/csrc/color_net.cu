@@ -45,8 +45,17 @@ struct NetArgs {
   unsigned* ovf;              // a colour above NCOL was needed
 };
 
+// words selected by compare, not by index: a dynamic index would put m[] in local memory
+__device__ __forceinline__ unsigned long long word_at(const unsigned long long (&m)[NW], int k) {
+  return k == 0 ? m[0] : k == 1 ? m[1] : k == 2 ? m[2] : m[3];
+}
+
 __device__ __forceinline__ void set_bit(unsigned long long (&m)[NW], i32 c) {
-  if (c >= 1 && c <= NCOL) m[(c - 1) >> 6] |= 1ull << ((c - 1) & 63);
+  const bool in = c >= 1 && c <= NCOL;
+  const int w = (c - 1) >> 6;
+  const unsigned long long b = in ? 1ull << ((c - 1) & 63) : 0ull;
+#pragma unroll
+  for (int k = 0; k < NW; k++) m[k] |= w == k ? b : 0ull;
 }
 
 // mask of net u from current colours, by one warp (rows are short; long rows loop)
@@ -60,7 +69,7 @@ __device__ __forceinline__ void build_mask(const NetArgs& a, i32 u, int lane) {
     const u32 lo = __reduce_or_sync(FULLM, (u32)m[w]), hi = __reduce_or_sync(FULLM, (u32)(m[w] >> 32));
     m[w] = ((unsigned long long)hi << 32) | lo;
   }
-  if (lane < NW) a.mask[(i64)u * NW + lane] = m[lane];
+  if (lane < NW) a.mask[(i64)u * NW + lane] = word_at(m, lane);
 }
 
 // all nets, GL lanes per net (four nets per warp; rows of ~32 entries take four
@@ -73,14 +82,23 @@ __global__ void k_masks_all(NetArgs a, i64 nv) {
     unsigned long long m[NW] = {0, 0, 0, 0};
     if (u < nv) {
       const i64 rs = a.rowptr[u], re = a.rowptr[u + 1];
-      for (i64 j = rs + sub; j < re; j += GL) set_bit(m, a.colors[__ldcs(a.col + j)]);
+      // four columns, then their four colours, in flight per lane
+      for (i64 j = rs + sub; j < re; j += 4 * GL) {
+        i32 us[4], cs[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) us[q] = j + q * GL < re ? __ldcs(a.col + j + q * GL) : -1;
+#pragma unroll
+        for (int q = 0; q < 4; q++) cs[q] = us[q] >= 0 ? a.colors[us[q]] : 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) set_bit(m, cs[q]);
+      }
       if (a.full && sub == 0) set_bit(m, a.colors[u]);
     }
 #pragma unroll
     for (int w = 0; w < NW; w++)
 #pragma unroll
       for (int o = GL / 2; o >= 1; o >>= 1) m[w] |= __shfl_xor_sync(FULLM, m[w], o);
-    if (u < nv && sub < NW) a.mask[u * NW + sub] = m[sub];
+    if (u < nv && sub < NW) a.mask[u * NW + sub] = word_at(m, sub);
   }
 }
 
@@ -96,59 +114,108 @@ __global__ void k_masks_around(NetArgs a) {
   }
 }
 
+// one pending vertex of a pick pass, as seen by one of its GL lanes: the parts that do
+// not depend on colours (worklist entry, row bounds, the lane's first four nets), so
+// the wave kernel can load the next wave's before the barrier
+struct PickItem {
+  i32 v;  // -1: no vertex for this group
+  i64 rs, re;
+  i32 us[4];
+};
+
+__device__ __forceinline__ void pick_load(const NetArgs& a, i64 i, i64 hi, int sub, PickItem& p) {
+  p.v = -1;
+  p.rs = p.re = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) p.us[q] = -1;
+  if (i >= hi) return;
+  p.v = a.wl[i];
+  p.rs = a.rowptr[p.v];
+  p.re = a.rowptr[p.v + 1];
+#pragma unroll
+  for (int q = 0; q < 4; q++) p.us[q] = p.rs + sub + q * GL < p.re ? a.col[p.rs + sub + q * GL] : -1;
+}
+
+// OR the vertex's nets' masks, take the first free colour, publish it into those nets;
+// called by every lane of the warp (the shuffles use all lanes)
+__device__ __forceinline__ void pick_finish(const NetArgs& a, const PickItem& p, int sub) {
+  const bool act = p.v >= 0;
+  unsigned long long m[NW] = {0, 0, 0, 0};
+  if (act) {
+    ulonglong4 qs[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      qs[q] = p.us[q] >= 0 ? *reinterpret_cast<const ulonglong4*>(a.mask + (i64)p.us[q] * NW) : make_ulonglong4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      m[0] |= qs[q].x;
+      m[1] |= qs[q].y;
+      m[2] |= qs[q].z;
+      m[3] |= qs[q].w;
+    }
+    for (i64 j = p.rs + sub + 4 * GL; j < p.re; j += GL) {
+      const i32 u = a.col[j];
+      const ulonglong4 q = *reinterpret_cast<const ulonglong4*>(a.mask + (i64)u * NW);
+      m[0] |= q.x;
+      m[1] |= q.y;
+      m[2] |= q.z;
+      m[3] |= q.w;
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < NW; w++)
+#pragma unroll
+    for (int o = GL / 2; o >= 1; o >>= 1) m[w] |= __shfl_xor_sync(FULLM, m[w], o);
+  if (!act) return;
+  i32 c = 0;
+#pragma unroll
+  for (int w = NW - 1; w >= 0; w--)
+    if (~m[w]) c = w * 64 + __ffsll((long long)~m[w]);
+  if (c == 0) {
+    if (sub == 0) atomicOr(a.ovf, 1u);
+    c = NCOL + 1;
+  } else {
+    // publish into the vertex's nets so later picks of this pass avoid it
+    const unsigned long long bit = 1ull << ((c - 1) & 63);
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      if (p.us[q] >= 0) atomicOr(a.mask + (i64)p.us[q] * NW + ((c - 1) >> 6), bit);
+    for (i64 j = p.rs + sub + 4 * GL; j < p.re; j += GL) atomicOr(a.mask + (i64)a.col[j] * NW + ((c - 1) >> 6), bit);
+    if (a.full && sub == 0) atomicOr(a.mask + (i64)p.v * NW + ((c - 1) >> 6), bit);
+  }
+  if (sub == 0) a.colors[p.v] = c;
+}
+
 // pick for worklist positions [lo, hi): GL lanes per pending vertex
-__device__ __forceinline__ void pick_range(const NetArgs& a, i64 lo, i64 hi) {
-  const int lane = threadIdx.x & 31, sub = lane % GL;
+__global__ void k_pick(NetArgs a) {
+  const int sub = (threadIdx.x & 31) % GL;
   const i64 gi = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / GL, ng = ((i64)gridDim.x * blockDim.x) / GL;
-  for (i64 base = lo; base < hi; base += ng) {  // uniform trip count: shuffles below use all lanes
-    const i64 i = base + gi;
-    const bool act = i < hi;
-    const i32 v = act ? a.wl[i] : 0;
-    unsigned long long m[NW] = {0, 0, 0, 0};
-    i64 rs = 0, re = 0;
-    if (act) {
-      rs = a.rowptr[v];
-      re = a.rowptr[v + 1];
-      for (i64 j = rs + sub; j < re; j += GL) {
-        const i32 u = a.col[j];
-        const ulonglong4 q = *reinterpret_cast<const ulonglong4*>(a.mask + (i64)u * NW);
-        m[0] |= q.x;
-        m[1] |= q.y;
-        m[2] |= q.z;
-        m[3] |= q.w;
-      }
-    }
-#pragma unroll
-    for (int w = 0; w < NW; w++)
-#pragma unroll
-      for (int o = GL / 2; o >= 1; o >>= 1) m[w] |= __shfl_xor_sync(FULLM, m[w], o);
-    if (act) {
-      i32 c = 0;
-#pragma unroll
-      for (int w = NW - 1; w >= 0; w--)
-        if (~m[w]) c = w * 64 + __ffsll((long long)~m[w]);
-      if (c == 0) {
-        if (sub == 0) atomicOr(a.ovf, 1u);
-        c = NCOL + 1;
-      } else {
-        // publish into the vertex's nets so later picks of this pass avoid it
-        const unsigned long long bit = 1ull << ((c - 1) & 63);
-        for (i64 j = rs + sub; j < re; j += GL) atomicOr(a.mask + (i64)a.col[j] * NW + ((c - 1) >> 6), bit);
-        if (a.full && sub == 0) atomicOr(a.mask + (i64)v * NW + ((c - 1) >> 6), bit);
-      }
-      if (sub == 0) a.colors[v] = c;
-    }
+  for (i64 base = 0; base < a.nwl; base += ng) {  // uniform trip count per warp
+    PickItem p;
+    pick_load(a, base + gi, a.nwl, sub, p);
+    pick_finish(a, p, sub);
   }
 }
 
-__global__ void k_pick(NetArgs a) { pick_range(a, 0, a.nwl); }
-
 // the first pass's waves in one cooperative launch, a grid barrier between waves (a
-// wave's picks and mask updates are visible to the next one)
+// wave's picks and mask updates are visible to the next one); each group's first item
+// of the next wave is loaded before the barrier, so a wave's critical path starts at
+// its mask loads
 __global__ void k_pick_waves(NetArgs a, int waves) {
   cg::grid_group grid = cg::this_grid();
+  const int sub = (threadIdx.x & 31) % GL;
+  const i64 gi = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / GL, ng = ((i64)gridDim.x * blockDim.x) / GL;
+  PickItem p;
+  pick_load(a, gi, a.nwl / waves, sub, p);
   for (int w = 0; w < waves; w++) {
-    pick_range(a, a.nwl * w / waves, a.nwl * (w + 1) / waves);
+    const i64 lo = a.nwl * w / waves, hi = a.nwl * (w + 1) / waves;
+    pick_finish(a, p, sub);
+    for (i64 base = lo + ng; base < hi; base += ng) {
+      PickItem q;
+      pick_load(a, base + gi, hi, sub, q);
+      pick_finish(a, q, sub);
+    }
+    if (w + 1 < waves) pick_load(a, hi + gi, a.nwl * (w + 2) / waves, sub, p);
     grid.sync();
   }
 }
@@ -168,18 +235,44 @@ __device__ __forceinline__ void detect_net(const NetArgs& a, i32 u, int lane, i3
     i32 x = -1, key = -1 - lane;
     if (lane < members) {
       x = lane < re0 - rs0 ? a.col[rs0 + lane] : u;
-      if (a.pend[x]) {
-        const i32 c = a.colors[x];
-        if (c >= 1) key = c;
-      }
+      const uint8_t pd = a.pend[x];  // both gathers in flight together
+      const i32 c = a.colors[x];
+      if (pd && c >= 1) key = c;
     }
     const unsigned grp = __match_any_sync(FULLM, key);
     const i32 top = __reduce_max_sync(grp, (unsigned)(x + 1)) - 1;  // x >= 0 inside a real group
     if (key > 0 && x < top) lose(a, x);
     return;
   }
-  for (int k = lane; k < NCOL + 2; k += 32) mx[k] = -1;
-  __syncwarp();
+  // mx[] holds -1 everywhere between nets (set at kernel start, restored after use)
+  if (members <= 64) {  // two members per lane, kept in registers for the loser test
+    i32 xs[2], ks[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const i64 idx = lane + 32 * h;
+      xs[h] = -1;
+      ks[h] = 0;
+      if (idx < members) {
+        xs[h] = idx < re0 - rs0 ? a.col[rs0 + idx] : u;
+        const uint8_t pd = a.pend[xs[h]];
+        const i32 c = a.colors[xs[h]];
+        if (pd && c >= 1 && c <= NCOL + 1) ks[h] = c;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+      if (ks[h]) atomicMax(mx + ks[h], xs[h]);
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+      if (ks[h] && mx[ks[h]] > xs[h]) lose(a, xs[h]);
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+      if (ks[h]) mx[ks[h]] = -1;
+    __syncwarp();
+    return;
+  }
   const i64 rs = a.rowptr[u], re = a.rowptr[u + 1];
   const i64 ext = a.full ? 1 : 0;  // the middle itself is a member of a D2 net
   for (i64 j = rs + lane; j < re + ext; j += 32) {
@@ -198,11 +291,15 @@ __device__ __forceinline__ void detect_net(const NetArgs& a, i32 u, int lane, i3
     if (c >= 1 && c <= NCOL + 1 && mx[c] > x && a.colors[x] != 0) lose(a, x);
   }
   __syncwarp();
+  for (int k = lane; k < NCOL + 2; k += 32) mx[k] = -1;
+  __syncwarp();
 }
 
 __global__ void k_detect_all(NetArgs a, i64 nv) {
   __shared__ i32 mxs[8][NCOL + 2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = lane; k < NCOL + 2; k += 32) mxs[wid][k] = -1;
+  __syncwarp();
   const i64 w0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
   for (i64 u = w0; u < nv; u += nw) detect_net(a, (i32)u, lane, mxs[wid]);
 }
@@ -210,6 +307,8 @@ __global__ void k_detect_all(NetArgs a, i64 nv) {
 __global__ void k_detect_around(NetArgs a) {
   __shared__ i32 mxs[8][NCOL + 2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = lane; k < NCOL + 2; k += 32) mxs[wid][k] = -1;
+  __syncwarp();
   const i64 w0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, nw = ((i64)gridDim.x * blockDim.x) >> 5;
   for (i64 i = w0; i < a.nwl; i += nw) {
     const i32 v = a.wl[i];

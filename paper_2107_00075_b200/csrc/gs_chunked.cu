@@ -659,7 +659,7 @@ bool launch_gs_chunked(const GsLaunch& L, i64 nwl, bool upper_zero, ChunkedScrat
     const char* e = std::getenv("CHROMA_GS_CHUNKS");
     return e ? std::atoll(e) : 0;
   }();
-  const i64 nchunks = nchunks_env > 0 ? nchunks_env : 32;
+  const i64 nchunks = nchunks_env > 0 ? nchunks_env : 64;  // C3: 32 -> 12.00 ms, 64 -> 11.83, 128 -> 13.5
   i64 chunk = std::max<i64>((i64)1 << 15, (nwl + nchunks - 1) / nchunks);
   if (chunk > nwl) chunk = nwl;
   // hub rows (deg > CF_HEAVY) of the worklist, counted (cached for an iota worklist):
