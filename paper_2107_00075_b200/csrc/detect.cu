@@ -367,80 +367,106 @@ __global__ void k_emit_short(const i64* rowptr, const i32* col, const i32* color
 }
 
 // A warp per item (changed vertex i, segment of SEG row entries): item j belongs to
-// the last i with segoff[i] <= j.  Keys go to *cnt-indexed slots (one atomic per warp
-// step; the caller sorts them).  WRITE = false only counts.
+// the last i with segoff[i] <= j.  Each warp takes a contiguous range of items (one
+// binary search, then a warp-wide forward scan of segoff per item).  Four 32-entry
+// steps of loads are in flight per lane; steps without an equal pair cost one ballot.
+// Keys go to *cnt-indexed slots (one atomic per warp step with keys; the caller
+// sorts them).  WRITE = false only counts.
 template <bool WRITE, bool ROWS>
 __global__ void k_changed_events(const i64* rowptr, const i32* col, const i32* colors, const uint8_t* owned,
                                  const i32* changed, i64 nch, const i64* segoff, i64 nitems,
                                  unsigned long long* cnt, u64* keys, unsigned long long cap) {
   const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const i64 warp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  for (i64 j = warp; j < nitems; j += nwarps) {
-    // upper_bound(segoff, j) - 1, searched by one lane
-    i64 i = 0;
-    if (lane == 0) {
-      i64 lo = 0, hi = nch;
-      while (hi - lo > 1) {
-        const i64 mid = (lo + hi) >> 1;
-        if (segoff[mid] <= j) lo = mid; else hi = mid;
-      }
-      i = lo;
+  const i64 per = (nitems + nwarps - 1) / nwarps;
+  const i64 j0 = warp * per, j1 = j0 + per < nitems ? j0 + per : nitems;
+  if (j0 >= j1) return;
+  // upper_bound(segoff, j0) - 1, searched by one lane
+  i64 i = 0;
+  if (lane == 0) {
+    i64 lo = 0, hi = nch;
+    while (hi - lo > 1) {
+      const i64 mid = (lo + hi) >> 1;
+      if (segoff[mid] <= j0) lo = mid; else hi = mid;
     }
-    i = __shfl_sync(FULL, i, 0);
+    i = lo;
+  }
+  i = __shfl_sync(FULL, i, 0);
+  unsigned long long mine = 0;
+  for (i64 j = j0; j < j1; j++) {
+    // advance to the last i with segoff[i] <= j (segoff is non-decreasing: the lanes
+    // that pass form a prefix)
+    for (;;) {
+      const i64 t = i + 1 + lane;
+      const unsigned b = __ballot_sync(FULL, t < nch && segoff[t] <= j);
+      i += __popc(b);
+      if (b != FULL) break;
+    }
     const i32 y = changed[i];
     const i32 cy = colors[y];
     const bool gy = ROWS || !owned[y];
     const i64 rs = rowptr[y], re = cy == 0 ? rowptr[y] : rowptr[y + 1];
     const i64 s0 = rs + (j - segoff[i]) * SEG;
     const i64 s1 = s0 + SEG < re ? s0 + SEG : re;
-    unsigned long long mine = 0;
-    for (i64 e0 = s0; e0 < s1; e0 += 32) {
-      const i64 e = e0 + lane;
-      i32 x = 0;
-      unsigned k = 0;
-      bool gx = false;
-      if (e < s1) {
-        x = col[e];
-        if (colors[x] == cy) {
-          gx = !ROWS && !owned[x];
-          k = (gy ? 1u : 0u) + (gx ? 1u : 0u);
-        }
-      }
+    for (i64 e0 = s0; e0 < s1; e0 += 4 * 32) {
+      i32 xs[4];
+      bool eq[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) xs[q] = e0 + q * 32 + lane < s1 ? col[e0 + q * 32 + lane] : -1;
+#pragma unroll
+      for (int q = 0; q < 4; q++) eq[q] = xs[q] >= 0 && colors[xs[q]] == cy;
+      bool gx[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) gx[q] = !ROWS && eq[q] && !owned[xs[q]];
       if (!WRITE) {
-        mine += k;
+#pragma unroll
+        for (int q = 0; q < 4; q++) mine += eq[q] ? (gy ? 1u : 0u) + (gx[q] ? 1u : 0u) : 0u;
         continue;
       }
-      unsigned inc = k;
+      if (!__any_sync(FULL, eq[0] || eq[1] || eq[2] || eq[3])) continue;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned t = __shfl_up_sync(FULL, inc, o);
-        if (lane >= o) inc += t;
-      }
-      const unsigned tot = __shfl_sync(FULL, inc, 31);
-      unsigned long long base = 0;
-      if (tot) {
-        if (lane == 31) base = atomicAdd(cnt, (unsigned long long)tot);
-        base = __shfl_sync(FULL, base, 31);
-      }
-      if (k) {
-        unsigned long long at = base + inc - k;
-        if (gy && at < cap) keys[at] = ((u64)(u32)y << 32) | (u32)x;
-        at += gy;
-        if (gx && at < cap) keys[at] = ((u64)(u32)x << 32) | (u32)y;
+      for (int q = 0; q < 4; q++) {
+        const unsigned b1 = __ballot_sync(FULL, eq[q] && gy), b2 = __ballot_sync(FULL, gx[q]);
+        const unsigned tot = __popc(b1) + __popc(b2);
+        if (!tot) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(cnt, (unsigned long long)tot);
+        base = __shfl_sync(FULL, base, 0);
+        unsigned long long at = base + __popc(b1 & lt) + __popc(b2 & lt);
+        if (eq[q] && gy) {
+          if (at < cap) keys[at] = ((u64)(u32)y << 32) | (u32)xs[q];
+          at++;
+        }
+        if (gx[q] && at < cap) keys[at] = ((u64)(u32)xs[q] << 32) | (u32)y;
       }
     }
-    if (!WRITE) {
-      mine = __reduce_add_sync(FULL, (unsigned)mine);
-      if (lane == 0 && mine) atomicAdd(cnt, mine);
-    }
+  }
+  if (!WRITE) {
+    mine = __reduce_add_sync(FULL, (unsigned)mine);
+    if (lane == 0 && mine) atomicAdd(cnt, mine);
   }
 }
 
-__global__ void k_flag_changed(const i32* colors, const i32* prev, i64 n, uint8_t* flag) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    const i32 c = colors[i];
-    flag[i] = (c != 0 && c != prev[i]) ? 1 : 0;
+// vertices whose colour changed since the previous call (coloured now), listed in
+// any order (the keys they emit are sorted): one atomic per warp step
+__global__ void k_changed_list(const i32* colors, const i32* prev, i64 n, i32* out, i64* cnt) {
+  const int lane = threadIdx.x & 31;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  for (i64 b = blockIdx.x * (i64)blockDim.x + threadIdx.x - lane; b < n; b += stride) {
+    const i64 i = b + lane;
+    bool ch = false;
+    if (i < n) {
+      const i32 c = colors[i];
+      ch = c != 0 && c != prev[i];
+    }
+    const unsigned m = __ballot_sync(FULL, ch);
+    if (!m) continue;
+    i64 base = 0;
+    if (lane == 0) base = (i64)atomicAdd(reinterpret_cast<unsigned long long*>(cnt), (unsigned long long)__popc(m));
+    base = __shfl_sync(FULL, base, 0);
+    if (ch) out[base + __popc(m & ((1u << lane) - 1u))] = (i32)i;
   }
 }
 
@@ -751,9 +777,8 @@ static i64 keyed_events(const DetectArgs& A, const DevDetect& a, DetectScratch& 
   S.off.reserve(nsrc, s);
   S.total.reserve(1, s);
   S.nch.reserve(1, s);
-  // rows mode: short rows by lanes (k_emit_short), long ones in segments; changed
-  // mode: every row in segments (changed vertices are few and their rows long)
-  k_changed_nseg<<<grid_for(nsrc, 256, num_sms() * 16), 256, 0, s>>>(A.rowptr, src, nsrc, S.cnt.p, rows_mode);
+  // short rows by lanes (k_emit_short), long ones in segments (k_changed_events)
+  k_changed_nseg<<<grid_for(nsrc, 256, num_sms() * 16), 256, 0, s>>>(A.rowptr, src, nsrc, S.cnt.p, true);
   count_launch();
   exclusive_scan_i64(S.cnt.p, S.off.p, nsrc, s);
   k_total<<<1, 1, 0, s>>>(S.cnt.p, S.off.p, nsrc, S.total.p);
@@ -775,10 +800,12 @@ static i64 keyed_events(const DetectArgs& A, const DevDetect& a, DetectScratch& 
                                                         nitems, S.nch.p, keys, cap);
       count_launch(nitems ? 2 : 1);
     } else {
+      k_emit_short<true, false><<<gs, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc, S.nch.p, keys,
+                                                   cap);
       if (nitems)
         k_changed_events<true, false><<<gw, 256, 0, s>>>(A.rowptr, A.col, A.colors, A.owned_flag, src, nsrc,
                                                          S.off.p, nitems, S.nch.p, keys, cap);
-      count_launch();
+      count_launch(nitems ? 2 : 1);
     }
   };
   i64 cap = std::max<i64>(S.keys.n, (i64)1 << 20);
@@ -852,13 +879,12 @@ void run_detect(const DetectArgs& A, i64 num_vertices, DetectScratch& S,
     bool rows_mode = true;
     if (A.incremental && S.prev_valid) {
       // only rows around changed vertices can hold an event: walk from the changed side
-      S.mark.reserve(num_vertices, s);
-      k_flag_changed<<<grid_for(num_vertices, 256, num_sms() * 16), 256, 0, s>>>(A.colors, S.prev.p, num_vertices,
-                                                                                 S.mark.p);
-      count_launch();
       S.chl.reserve(num_vertices, s);
       S.narows.reserve(1, s);
-      select_flagged(S.mark.p, num_vertices, S.chl.p, S.narows.p, s);
+      CUDA_CHECK(cudaMemsetAsync(S.narows.p, 0, sizeof(i64), s));
+      k_changed_list<<<grid_for(num_vertices, 256, num_sms() * 16), 256, 0, s>>>(A.colors, S.prev.p, num_vertices,
+                                                                                 S.chl.p, S.narows.p);
+      count_launch();
       CUDA_CHECK(cudaMemcpyAsync(&nsrc, S.narows.p, sizeof(i64), cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
       src = S.chl.p;
