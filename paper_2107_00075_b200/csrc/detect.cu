@@ -239,28 +239,41 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nb) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024, 1) k_resolve_grid(const int2* ev, i64 E, uint8_t* fired, i32* kill,
-                                                          i32* colors, unsigned long long* conflicts, unsigned* bar,
-                                                          int* changed) {
+// kill64[v] = (tag(sweep) << 32 | smallest fired event with loser v) for the current
+// sweep; a value with another sweep's tag reads as "no kill", so the per-sweep reset
+// pass (and its barrier) of k_resolve is not needed.  Tags fall as sweeps advance, so
+// the sweep's atomicMin always replaces an older value.
+__device__ __forceinline__ unsigned long long kill_tag(i64 it) { return 0xFFFFFFFEull - (unsigned long long)it; }
+
+__device__ __forceinline__ i32 kill_read(const unsigned long long* kill, i32 v, unsigned long long tag) {
+  const unsigned long long k = kill[v];
+  return (k >> 32) == tag ? (i32)(u32)k : INT32_MAX;
+}
+
+__global__ void __launch_bounds__(1024, 1) k_resolve_grid(const int2* ev, i64 E, uint8_t* fired,
+                                                          unsigned long long* kill, i32* colors,
+                                                          unsigned long long* conflicts, unsigned* bar, int* changed) {
   const i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x, T = (i64)gridDim.x * blockDim.x;
   const unsigned nb = gridDim.x;
-  for (i64 e = t; e < E; e += T) fired[e] = 1;
+  for (i64 e = t; e < E; e += T) {
+    fired[e] = 1;
+    kill[ev[e].x] = ~0ull;  // a tag no sweep uses
+    kill[ev[e].y] = ~0ull;
+  }
+  grid_sync(bar, nb);
   for (i64 it = 0; it <= E + 1; it++) {
     // three flags: this sweep's, the next one's (cleared now), and the previous
     // one's, which a block that just left the last barrier may still be reading
     int* ch = changed + it % 3;
     if (t == 0) changed[(it + 1) % 3] = 0;
-    for (i64 e = t; e < E; e += T) {
-      kill[ev[e].x] = INT32_MAX;
-      kill[ev[e].y] = INT32_MAX;
-    }
-    grid_sync(bar, nb);
+    const unsigned long long tag = kill_tag(it);
     for (i64 e = t; e < E; e += T)
-      if (fired[e]) atomicMin(&kill[ev[e].x], (i32)e);
+      if (fired[e]) atomicMin(kill + ev[e].x, (tag << 32) | (u32)e);
     grid_sync(bar, nb);
     bool mine = false;
     for (i64 e = t; e < E; e += T) {
-      const uint8_t f = (kill[ev[e].x] >= (i32)e && kill[ev[e].y] >= (i32)e) ? 1 : 0;
+      const int2 q = ev[e];
+      const uint8_t f = (kill_read(kill, q.x, tag) >= (i32)e && kill_read(kill, q.y, tag) >= (i32)e) ? 1 : 0;
       if (f != fired[e]) {
         fired[e] = f;
         mine = true;
@@ -968,7 +981,8 @@ static void resolve_events(const DetectArgs& A, DetectScratch& S, i64 E, unsigne
     int* changed = reinterpret_cast<int*>(S.result.p + 1);
     const int2* evp = S.ev.p;
     uint8_t* fp = S.fired.p;
-    i32* kp = S.kill.p;
+    S.kill64.reserve(num_vertices, s);
+    unsigned long long* kp = S.kill64.p;
     i32* cp = A.colors;
     void* args[] = {(void*)&evp, (void*)&E, (void*)&fp, (void*)&kp, (void*)&cp, (void*)&conflicts_dev, (void*)&bar,
                     (void*)&changed};

@@ -198,6 +198,7 @@ struct DetectScratch {
   DBuf<int2> ev;
   DBuf<uint8_t> fired;
   DBuf<i32> kill;
+  DBuf<unsigned long long> kill64;  // grid resolve: (sweep tag << 32 | event) per vertex
   DBuf<unsigned long long> result;  // [0] conflicts
   DBuf<i64> total;
   // incremental mode: colours at the end of the previous detection, row marks
