@@ -129,12 +129,11 @@ __device__ __forceinline__ void pick_load(const NetArgs& a, i64 i, i64 hi, int s
 #pragma unroll
   for (int q = 0; q < 4; q++) p.us[q] = -1;
   if (i >= hi) return;
-  // streaming loads (evict first): the L2 is kept for the masks the waves gather
-  p.v = __ldcs(a.wl + i);
-  p.rs = __ldcs(a.rowptr + p.v);
-  p.re = __ldcs(a.rowptr + p.v + 1);
+  p.v = a.wl[i];
+  p.rs = a.rowptr[p.v];
+  p.re = a.rowptr[p.v + 1];
 #pragma unroll
-  for (int q = 0; q < 4; q++) p.us[q] = p.rs + sub + q * GL < p.re ? __ldcs(a.col + p.rs + sub + q * GL) : -1;
+  for (int q = 0; q < 4; q++) p.us[q] = p.rs + sub + q * GL < p.re ? a.col[p.rs + sub + q * GL] : -1;
 }
 
 // OR the vertex's nets' masks, take the first free colour, publish it into those nets;
