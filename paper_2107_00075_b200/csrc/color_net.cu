@@ -231,20 +231,24 @@ __device__ __forceinline__ void lose(const NetArgs& a, i32 x) {
 __device__ __forceinline__ void detect_net(const NetArgs& a, i32 u, int lane, i32* mx) {
   const i64 rs0 = a.rowptr[u], re0 = a.rowptr[u + 1];
   const i64 members = re0 - rs0 + (a.full ? 1 : 0);
-  if (members <= 32) {  // one member per lane: equal-colour groups by __match_any_sync
-    i32 x = -1, key = -1 - lane;
+  // mx[] holds -1 everywhere between nets (set at kernel start, restored after use)
+  if (members <= 32) {  // one member per lane: the largest pending id per colour in mx[]
+    i32 x = -1, key = 0;
     if (lane < members) {
       x = lane < re0 - rs0 ? a.col[rs0 + lane] : u;
       const uint8_t pd = a.pend[x];  // both gathers in flight together
       const i32 c = a.colors[x];
-      if (pd && c >= 1) key = c;
+      if (pd && c >= 1 && c <= NCOL + 1) key = c;
     }
-    const unsigned grp = __match_any_sync(FULLM, key);
-    const i32 top = __reduce_max_sync(grp, (unsigned)(x + 1)) - 1;  // x >= 0 inside a real group
-    if (key > 0 && x < top) lose(a, x);
+    if (key) atomicMax(mx + key, x);
+    __syncwarp();
+    const bool l = key && mx[key] > x;
+    __syncwarp();
+    if (key) mx[key] = -1;
+    __syncwarp();
+    if (l) lose(a, x);
     return;
   }
-  // mx[] holds -1 everywhere between nets (set at kernel start, restored after use)
   if (members <= 64) {  // two members per lane, kept in registers for the loser test
     i32 xs[2], ks[2];
 #pragma unroll
